@@ -1,0 +1,126 @@
+"""Seeded synthetic inputs for the decode hot path (host / numpy side).
+
+This module holds NO arithmetic of the method: it only draws the inputs the
+paper's workload has:
+
+* K, V ~ N(0, 1) rounded to bf16 (SPEC S:375 key/value generator);
+* query windows follow SPEC's AR(1) trace q_t = 0.95 q_{t-1} + 0.05 xi_t
+   for W steps; the current query q is step W, rounded to bf16.
+
+Every value is a pure function of (seed, stream, global index), computed with
+integer arithmetic plus IEEE round-to-nearest fp32 multiply/add only, so the
+device generator in ``csrc/synth.cu`` reproduces it bit for bit (checked by
+tests/test_gpu_parity.py::test_device_generator_matches_host).  Both the
+oracle side (tests) and the CUDA side (tests, bench) draw from this one
+definition; nothing here depends on either.
+
+Normal deviates: Irwin-Hall(4) of four 16-bit lanes of a splitmix64 hash,
+centred and scaled to unit variance (support +-3.46 sigma) -- an exactly
+reproducible stand-in for Box-Muller, whose transcendental functions differ
+between libm and CUDA.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+M64 = (1 << 64) - 1
+GOLDEN = 0x9E3779B97F4A7C15
+STREAM_K, STREAM_V, STREAM_Q = 1, 2, 3
+NORM_SCALE = np.float32(1.0 / 37837.22668)   # 1 / std of a sum of four U{0..65535}
+NORM_MEAN = 131070                            # 4 * 65535 / 2
+AR_ALPHA = np.float32(0.95)
+AR_SIGMA = np.float32(0.05)
+
+
+def base_seed(config_index: int, repetition: int = 0) -> int:
+    """seed = 20251008 + 1000 * config_index + repetition."""
+    return 20251008 + 1000 * config_index + repetition
+
+
+def _splitmix64_scalar(x: int) -> int:
+    z = (x + GOLDEN) & M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def stream_key(seed: int, stream: int) -> int:
+    return _splitmix64_scalar((seed ^ (stream << 48)) & M64)
+
+
+def _splitmix64(x: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        z = x + np.uint64(GOLDEN)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def normal_from_index(seed: int, stream: int, idx: np.ndarray) -> np.ndarray:
+    """fp32 N(0,1)-like deviate for each uint64 global index."""
+    with np.errstate(over="ignore"):
+        z = _splitmix64(np.uint64(stream_key(seed, stream)) + idx.astype(np.uint64))
+    m = np.uint64(0xFFFF)
+    s = ((z & m) + ((z >> np.uint64(16)) & m) + ((z >> np.uint64(32)) & m)
+         + (z >> np.uint64(48))).astype(np.int64) - NORM_MEAN
+    return s.astype(np.float32) * NORM_SCALE          # exact int->fp32, one RN multiply
+
+
+def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even fp32 -> bf16 bit pattern (finite inputs)."""
+    b = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    r = (b + np.uint64(0x7FFF) + ((b >> np.uint64(16)) & np.uint64(1))) >> np.uint64(16)
+    return r.astype(np.uint16)
+
+
+def bf16_bits_to_f32(h: np.ndarray) -> np.ndarray:
+    return (np.asarray(h, np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32)
+
+
+def kv_rows(seed: int, stream: int, b: int, h: int, t0: int, t1: int, n_kv_heads: int,
+            max_len: int, head_dim: int) -> np.ndarray:
+    """bf16 bits [t1-t0, D] of K (stream 1) or V (stream 2) for GLOBAL batch b,
+    GLOBAL kv head h, tokens [t0, t1)."""
+    t = np.arange(t0, t1, dtype=np.uint64)[:, None]
+    d = np.arange(head_dim, dtype=np.uint64)[None, :]
+    idx = ((np.uint64(b) * np.uint64(n_kv_heads) + np.uint64(h)) * np.uint64(max_len) + t) \
+        * np.uint64(head_dim) + d
+    return f32_to_bf16_bits(normal_from_index(seed, stream, idx))
+
+
+def kv_cache(seed: int, stream: int, batch: int, n_kv_heads: int, max_len: int, head_dim: int,
+             b0: int = 0, h0: int = 0, n_kv_heads_global: int | None = None,
+             batch_slice: int | None = None, head_slice: int | None = None) -> np.ndarray:
+    """bf16 bits [B_s, H_s, L, D]; a shard (b0.., h0..) of the global tensor."""
+    hg = n_kv_heads if n_kv_heads_global is None else n_kv_heads_global
+    bs = batch if batch_slice is None else batch_slice
+    hs = n_kv_heads if head_slice is None else head_slice
+    out = np.empty((bs, hs, max_len, head_dim), np.uint16)
+    for i in range(bs):
+        for j in range(hs):
+            out[i, j] = kv_rows(seed, stream, b0 + i, h0 + j, 0, max_len, hg, max_len, head_dim)
+    return out
+
+
+def query_trace(seed: int, batch: int, n_q_heads: int, window: int, head_dim: int,
+                b0: int = 0, h0: int = 0, n_q_heads_global: int | None = None,
+                batch_slice: int | None = None, head_slice: int | None = None):
+    """AR(1) query trace: returns (window fp32 [B_s, H_s, W, D] in
+    logical order oldest..newest, q bf16 bits [B_s, H_s, D] = step W)."""
+    hg = n_q_heads if n_q_heads_global is None else n_q_heads_global
+    bs = batch if batch_slice is None else batch_slice
+    hs = n_q_heads if head_slice is None else head_slice
+    T = window + 1
+    b = np.arange(b0, b0 + bs, dtype=np.uint64)[:, None, None, None]
+    h = np.arange(h0, h0 + hs, dtype=np.uint64)[None, :, None, None]
+    t = np.arange(T, dtype=np.uint64)[None, None, :, None]
+    d = np.arange(head_dim, dtype=np.uint64)[None, None, None, :]
+    idx = ((b * np.uint64(hg) + h) * np.uint64(T) + t) * np.uint64(head_dim) + d
+    xi = normal_from_index(seed, STREAM_Q, idx)
+    qs = np.empty_like(xi)
+    qs[:, :, 0] = xi[:, :, 0]
+    for s in range(1, T):
+        a = (AR_ALPHA * qs[:, :, s - 1]).astype(np.float32)
+        e = (AR_SIGMA * xi[:, :, s]).astype(np.float32)
+        qs[:, :, s] = (a + e).astype(np.float32)
+    return np.ascontiguousarray(qs[:, :, :window]), f32_to_bf16_bits(qs[:, :, window])

@@ -1,0 +1,406 @@
+"""Pins for the CPU oracle (oracle/asp_oracle.c) -- checks it against what the
+paper and mathematics fix, never against itself: closed forms, special cases,
+invariants, brute force and independent library routines (numpy).  Each test
+names the passage / SURVEY §8(c) reading it pins.  CPU only."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2510_07486_b200 import synth
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+MODES = [oracle.ASSEMBLY_MASKED_SHARED, oracle.ASSEMBLY_SINGLE, oracle.ASSEMBLY_PER_WINDOW,
+         oracle.ASSEMBLY_MASKED_SHARED | oracle.DOUBLE_SOFTMAX]
+
+
+def _softmax(v):
+    v = np.asarray(v, np.float64)
+    e = np.exp(v - v.max())
+    return e / e.sum()
+
+
+# ----------------------------------------------------------------------------- predict
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("W", [2, 4, 16])
+def test_constant_window_is_exact(mode, W):
+    """a constant window predicts the constant, bit-exactly
+    (every candidate is a convex combination of identical vectors)."""
+    rng = np.random.default_rng(1)
+    q = rng.standard_normal(64).astype(np.float32)
+    win = np.broadcast_to(q, (3, W, 64)).copy()
+    qh, cond = oracle.predict(win, 1e-2, mode)
+    assert cond == 0
+    assert np.array_equal(qh, np.broadcast_to(q, (3, 64)))
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_w2_returns_newest(mode):
+    """W = 2 leaves one usable weight, so q_hat = Q_t in
+    every mode (masked-shared == per-window at W = 2)."""
+    rng = np.random.default_rng(2)
+    win = rng.standard_normal((5, 2, 32)).astype(np.float32)
+    qh, _ = oracle.predict(win, 1e-2, mode)
+    assert np.array_equal(qh, win[:, 1])
+
+
+def test_w1_passthrough():
+    """S:208 warm-up rule: fewer than two queries -> passthrough."""
+    win = np.random.default_rng(3).standard_normal((2, 1, 16)).astype(np.float32)
+    qh, _ = oracle.predict(win)
+    assert np.array_equal(qh, win[:, 0])
+
+
+def test_large_eps_closed_form_masked_shared():
+    """Readings R3-R6 pinned by a closed form: with eps -> infinity the ridge
+    weights vanish, every row softmax is uniform over its n_j = min(j, W-1)
+    entries, so q_hat = (1/W) sum_j mean(Q[W-n_j..W-1]).  (NOT the window
+    mean that S:202 claims -- it differs.)"""
+    rng = np.random.default_rng(4)
+    W, D = 8, 48
+    win = rng.standard_normal((6, W, D)).astype(np.float32)
+    qh, _ = oracle.predict(win, 1e12, oracle.ASSEMBLY_MASKED_SHARED)
+    Q = win.astype(np.float64)
+    n = W - 1
+    exp = np.zeros((6, D))
+    for j in range(1, W + 1):
+        nj = min(j, n)
+        exp += Q[:, W - nj:].mean(axis=1)
+    exp /= W
+    np.testing.assert_allclose(qh, exp, rtol=0, atol=1e-6)
+    assert np.abs(exp - Q.mean(axis=1)).max() > 1e-2   # S:202's "window mean" is wrong
+
+
+def test_large_eps_closed_form_single_and_per_window():
+    """Eq. 4 with uniform weights: mean(Q[1..W-1]); Eq. 5 literal
+    (m = W-1): (1/n) sum_k mean(Q[W-k..W-1])."""
+    rng = np.random.default_rng(5)
+    W, D = 6, 40
+    win = rng.standard_normal((4, W, D)).astype(np.float32)
+    Q = win.astype(np.float64)
+    qs, _ = oracle.predict(win, 1e12, oracle.ASSEMBLY_SINGLE)
+    np.testing.assert_allclose(qs, Q[:, 1:].mean(axis=1), atol=1e-6, rtol=0)
+    qp, _ = oracle.predict(win, 1e12, oracle.ASSEMBLY_PER_WINDOW)
+    n = W - 1
+    exp = sum(Q[:, W - k:].mean(axis=1) for k in range(1, n + 1)) / n
+    np.testing.assert_allclose(qp, exp, atol=1e-6, rtol=0)
+
+
+def _orthonormal_window(W, D, a):
+    """History rows Q[0..n-1] = e_1..e_n, newest Q[W-1] = sum a_i e_i."""
+    n = W - 1
+    win = np.zeros((W, D), np.float32)
+    for i in range(n):
+        win[i, i] = 1.0
+    win[W - 1, :n] = a
+    return win
+
+
+@pytest.mark.parametrize("negated", [False, True])
+def test_orthonormal_history_closed_form(negated):
+    """Alg. 1 Step 3 pinned exactly: G0 = I, mean diag = 1, so with
+    relative eps = 1e-2 the ridge weights are omega = a / 1.01 (generalises
+    S:164).  Then every assembly mode has a closed-form softmax mixture."""
+    W, D = 5, 16
+    n = W - 1
+    a = np.array([0.5, -1.0, 2.0, 0.25], np.float32)
+    win = _orthonormal_window(W, D, a)
+    Q = win.astype(np.float64)
+    om = a.astype(np.float64) / 1.01
+    s = -1.0 if negated else 1.0
+    flag = oracle.SIGN_NEGATED if negated else 0
+    # masked-shared (R4/R5/R6)
+    exp = np.zeros(D)
+    for j in range(1, W + 1):
+        nj = min(j, n)
+        r = _softmax(s * om[:nj])
+        exp += r @ Q[W - nj:]
+    exp /= W
+    qh, _ = oracle.predict(win[None], 1e-2, oracle.ASSEMBLY_MASKED_SHARED | flag)
+    np.testing.assert_allclose(qh[0], exp, atol=1e-7, rtol=0)
+    # single (Eq. 4)
+    qs, _ = oracle.predict(win[None], 1e-2, oracle.ASSEMBLY_SINGLE | flag)
+    np.testing.assert_allclose(qs[0], _softmax(s * om) @ Q[1:], atol=1e-7, rtol=0)
+    # double softmax (literal Step 4)
+    p = _softmax(s * om)
+    exp2 = sum(_softmax(p[:min(j, n)]) @ Q[W - min(j, n):] for j in range(1, W + 1)) / W
+    qd, _ = oracle.predict(win[None], 1e-2,
+                           oracle.ASSEMBLY_MASKED_SHARED | oracle.DOUBLE_SOFTMAX | flag)
+    np.testing.assert_allclose(qd[0], exp2, atol=1e-7, rtol=0)
+    # per-window (Eq. 5): H_k = e_{n-k+1}..e_n -> omega_k = a[n-k:] / 1.01
+    exp3 = sum(_softmax(s * a[n - k:].astype(np.float64) / 1.01) @ Q[W - k:]
+               for k in range(1, n + 1)) / n
+    qp, _ = oracle.predict(win[None], 1e-2, oracle.ASSEMBLY_PER_WINDOW | flag)
+    np.testing.assert_allclose(qp[0], exp3, atol=1e-7, rtol=0)
+
+
+def test_sign_example_from_spec():
+    """softmax([ln 2, 0]) = [2/3, 1/3]; negated -> [1/3, 2/3].
+    Realised through SINGLE mode at W = 3 with absolute eps chosen so the
+    ridge weights are exactly [ln 2, 0] on an orthonormal history."""
+    ln2 = np.log(2.0)
+    win = np.zeros((3, 8), np.float32)
+    win[0, 0] = 1.0
+    win[1, 1] = 1.0
+    # omega = a / (1 + eps): pick a0 = ln2 * (1 + eps) in fp32 exactly enough
+    eps = 2.0 ** -20
+    win[2, 0] = np.float32(ln2 * (1 + eps))
+    qs, _ = oracle.predict(win[None], eps, oracle.ASSEMBLY_SINGLE | oracle.EPS_ABSOLUTE)
+    # weights (2/3, 1/3) applied to Q[1], Q[2]
+    exp = (2 / 3) * win[1].astype(np.float64) + (1 / 3) * win[2].astype(np.float64)
+    np.testing.assert_allclose(qs[0], exp, atol=2e-7)
+    qn, _ = oracle.predict(win[None], eps,
+                           oracle.ASSEMBLY_SINGLE | oracle.EPS_ABSOLUTE | oracle.SIGN_NEGATED)
+    exp = (1 / 3) * win[1].astype(np.float64) + (2 / 3) * win[2].astype(np.float64)
+    np.testing.assert_allclose(qn[0], exp, atol=2e-7)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_power_of_two_scale_equivariance(mode):
+    """S:199, S:307 scale equivariance; with relative eps a 2^k scaling is
+    exact in floating point, so q_hat scales bit-exactly."""
+    rng = np.random.default_rng(6)
+    win = rng.standard_normal((8, 16, 128)).astype(np.float32)
+    q1, _ = oracle.predict(win, 1e-2, mode)
+    q8, _ = oracle.predict(win * np.float32(8.0), 1e-2, mode)
+    assert np.array_equal(q8, q1 * np.float32(8.0))
+
+
+def test_raw_single_window_reproduces_exact_linear_recurrence():
+    """North star: 'the regressor reproduces exactly-linear query sequences'
+    (reading R17: the raw, NORM_NONE single-window ridge regression).  With an
+    exact order-(W-1) recurrence Q_s = sum_i c_i Q_{s-i} over dyadic c_i and
+    small-integer starts (exact in fp32), Eq. 4's shifted weights predict the
+    next element of the recurrence."""
+    rng = np.random.default_rng(7)
+    for trial in range(20):
+        W, D = 5, 64
+        n = W - 1
+        c = rng.choice([-0.5, -0.25, 0.25, 0.5, 0.125], size=n)
+        seq = [rng.integers(-3, 4, D).astype(np.float64) for _ in range(n)]
+        for _ in range(2):
+            seq.append(sum(c[i] * seq[-1 - i] for i in range(n)))
+        win = np.array(seq[:W], np.float32)
+        assert np.array_equal(win.astype(np.float64), np.array(seq[:W]))  # exact in fp32
+        qh, cond = oracle.predict(win[None], 1e-12,
+                                  oracle.ASSEMBLY_SINGLE | oracle.NORM_NONE | oracle.EPS_ABSOLUTE)
+        assert cond == 0
+        np.testing.assert_allclose(qh[0], seq[W], atol=1e-9 * (1 + np.abs(seq[W]).max()))
+
+
+@pytest.mark.parametrize("mode", [oracle.ASSEMBLY_MASKED_SHARED, oracle.ASSEMBLY_SINGLE,
+                                  oracle.ASSEMBLY_PER_WINDOW])
+def test_convexity(mode):
+    """S:143 / S:221: softmax modes output a convex combination of window
+    queries: ||q_hat|| <= max_p ||Q_p||."""
+    rng = np.random.default_rng(8)
+    win = rng.standard_normal((64, 16, 64)).astype(np.float32) * rng.uniform(
+        0.1, 10, (64, 16, 1)).astype(np.float32)
+    qh, _ = oracle.predict(win, 1e-2, mode)
+    assert np.all(np.linalg.norm(qh, axis=1)
+                  <= np.linalg.norm(win, axis=2).max(axis=1) * (1 + 1e-6))
+
+
+def test_ridge_solve_matches_numpy_linalg():
+    """Alg. 1 Step 3 via an independent library solve: numpy.linalg.solve of
+    (G0 + eps I) omega = beta, then the SINGLE-mode softmax mixture."""
+    for W in (4, 9, 16):
+        win = synth.query_trace(123 + W, 4, 2, W, 128)[0].reshape(8, W, 128)
+        qs, _ = oracle.predict(win, 1e-2, oracle.ASSEMBLY_SINGLE)
+        for r in range(8):
+            Q = win[r].astype(np.float64)
+            H, y = Q[:-1], Q[-1]
+            G0 = H @ H.T
+            om = np.linalg.solve(G0 + 1e-2 * np.mean(np.diag(G0)) * np.eye(W - 1), H @ y)
+            np.testing.assert_allclose(qs[r], _softmax(om) @ Q[1:], rtol=0,
+                                       atol=1e-6 * np.abs(Q).max())
+
+
+def test_not_pd_and_nonfinite_passthrough():
+    """S:69 not-PD error class and S:208 passthrough: a negative absolute eps
+    on a zero history has a non-positive pivot -> flag 2, q_hat = newest; a
+    NaN window -> flag 1, passthrough."""
+    win = np.zeros((1, 4, 8), np.float32)
+    win[0, 3] = np.arange(8)
+    qh, cond = oracle.predict(win, -1.0, oracle.EPS_ABSOLUTE)
+    assert cond & oracle.FLAG_NOT_PD and np.array_equal(qh[0], win[0, 3])
+    win2 = np.ones((1, 4, 8), np.float32)
+    win2[0, 1, 2] = np.nan
+    qh2, cond2 = oracle.predict(win2)
+    assert cond2 & oracle.FLAG_NONFINITE and np.array_equal(qh2[0], win2[0, 3])
+
+
+def test_ring_start_rotation():
+    """Ring mapping (§8(b)): logical slot j lives at physical (ring_start+j)%W."""
+    rng = np.random.default_rng(10)
+    win = rng.standard_normal((3, 7, 32)).astype(np.float32)
+    q0, _ = oracle.predict(win)
+    rot = np.roll(win, 3, axis=1)        # physical[(3 + j) % W] = logical[j]
+    q3, _ = oracle.predict(rot, ring_start=3)
+    assert np.array_equal(q0, q3)
+
+
+# ----------------------------------------------------------------------------- score
+def _kv(rng, B, H, L, D):
+    return synth.f32_to_bf16_bits(rng.standard_normal((B, H, L, D)).astype(np.float32))
+
+
+def test_score_basis_query_reads_first_column():
+    """q_hat = e_1 -> score of token n = K[n, 0]."""
+    rng = np.random.default_rng(11)
+    K = _kv(rng, 2, 2, 50, 64)
+    q = np.zeros((2, 4, 64), np.float32)
+    q[..., 0] = 1.0
+    s, _ = oracle.score(q, K, 50)
+    np.testing.assert_array_equal(s, synth.bf16_bits_to_f32(K[..., 0]).astype(np.float64))
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_score_matches_numpy_matmul(G):
+    """Alg. 1 Step 7 with a library fp64 matmul per head, reduced
+    over the group by elementwise max (R10) or sum."""
+    rng = np.random.default_rng(12 + G)
+    B, Hkv, L, D = 2, 2, 97, 128
+    K = _kv(rng, B, Hkv, L, D)
+    q = rng.standard_normal((B, Hkv * G, D)).astype(np.float32)
+    s, _ = oracle.score(q, K, [97, 60])
+    s_sum, _ = oracle.score(q, K, [97, 60], oracle.AGG_SUM)
+    Kf = synth.bf16_bits_to_f32(K).astype(np.float64)
+    for b in range(B):
+        for h in range(Hkv):
+            per = Kf[b, h] @ q[b, h * G:(h + 1) * G].astype(np.float64).T   # [L, G]
+            ln = [97, 60][b]
+            np.testing.assert_allclose(s[b, h, :ln], per.max(axis=1)[:ln], rtol=1e-13, atol=1e-12)
+            np.testing.assert_allclose(s_sum[b, h, :ln], per.sum(axis=1)[:ln], rtol=1e-13,
+                                       atol=1e-12)
+            assert np.all(np.isneginf(s[b, h, ln:]))
+
+
+# ----------------------------------------------------------------------------- select
+def _brute_topk(s, k):
+    """Brute force: full lexicographic sort by (-score, index)."""
+    order = np.lexsort((np.arange(len(s)), -s))
+    return np.sort(order[:k])
+
+
+def test_select_matches_brute_force_with_ties():
+    """S:93, S:710 'top-k matches a brute-force full sort', with the north
+    star's lower-index tie-break (R9) -- scores drawn from a 16-value codebook
+    so exact ties are everywhere."""
+    rng = np.random.default_rng(13)
+    for L, k in [(1000, 100), (257, 32), (4096, 256), (64, 64)]:
+        s = rng.integers(0, 16, (6, L)).astype(np.float64) * 0.37
+        idx, cond = oracle.select(s, k)
+        for r in range(6):
+            np.testing.assert_array_equal(idx[r], _brute_topk(s[r], k))
+        s2 = rng.standard_normal((6, L))
+        idx2, _ = oracle.select(s2, k)
+        for r in range(6):
+            np.testing.assert_array_equal(idx2[r], _brute_topk(s2[r], k))
+
+
+def test_select_special_cases():
+    """S:282-283 and R9/R13: k = L -> identity; increasing -> last k; all
+    equal -> first k; positive scaling invariant; short rows padded."""
+    L = 300
+    ident, _ = oracle.select(np.random.default_rng(14).standard_normal(L), L)
+    np.testing.assert_array_equal(ident, np.arange(L))
+    inc, _ = oracle.select(np.arange(L, dtype=np.float64), 7)
+    np.testing.assert_array_equal(inc, np.arange(L - 7, L))
+    eq, _ = oracle.select(np.full(L, 3.5), 9)
+    np.testing.assert_array_equal(eq, np.arange(9))
+    s = np.random.default_rng(15).standard_normal(L)
+    np.testing.assert_array_equal(oracle.select(s, 20)[0], oracle.select(s * 7.25, 20)[0])
+    short, cond = oracle.select(np.arange(10, dtype=np.float64)[None], 16, [10])
+    assert cond & oracle.FLAG_SHORT_ROW
+    np.testing.assert_array_equal(short[0], list(range(10)) + [-1] * 6)
+
+
+def test_select_nan_sorts_last():
+    """R14: NaN scores rank below every number."""
+    s = np.array([1.0, np.nan, 0.5, -3.0, np.nan])
+    idx, cond = oracle.select(s, 3)
+    assert cond & oracle.FLAG_NONFINITE
+    np.testing.assert_array_equal(idx, [0, 2, 3])
+
+
+def test_select_spec_golden_examples():
+    """tests/golden/spec_select_examples.json: SPEC S:91-92 examples, the
+    tie case restated under the north-star tie-break (lower index wins)."""
+    with open(os.path.join(GOLDEN, "spec_select_examples.json")) as f:
+        cases = json.load(f)["cases"]
+    for c in cases:
+        idx, _ = oracle.select(np.array(c["scores"], np.float64), c["k"])
+        assert idx.tolist() == c["expect"], c
+
+
+# ----------------------------------------------------------------------------- decode
+def _attn_numpy(q, K, V, toks, scale):
+    """Library evaluation of softmax attention (fp64 numpy)."""
+    l = (K[toks] @ q) * scale
+    p = np.exp(l - l.max())
+    return (p / p.sum()) @ V[toks]
+
+
+def test_decode_matches_numpy_and_dense_at_full_selection():
+    """North star / S:310: with k = L (every token), sparse attention
+    equals dense attention; both equal a numpy fp64 evaluation."""
+    rng = np.random.default_rng(16)
+    B, Hq, Hkv, L, D = 2, 4, 2, 90, 64
+    K, V = _kv(rng, B, Hkv, L, D), _kv(rng, B, Hkv, L, D)
+    q = synth.f32_to_bf16_bits(rng.standard_normal((B, Hq, D)).astype(np.float32))
+    idx = np.broadcast_to(np.arange(L, dtype=np.int32), (B, Hkv, L)).copy()
+    out = oracle.sparse_decode(q, K, V, idx, L)
+    dense = oracle.dense_attention(q, K, V, L)
+    np.testing.assert_array_equal(out, dense)
+    Kf, Vf, qf = (synth.bf16_bits_to_f32(x).astype(np.float64) for x in (K, V, q))
+    for b in range(B):
+        for hq in range(Hq):
+            h = hq // (Hq // Hkv)
+            ref = _attn_numpy(qf[b, hq], Kf[b, h], Vf[b, h], np.arange(L), 1 / np.sqrt(D))
+            np.testing.assert_allclose(out[b, hq], ref, rtol=1e-6, atol=1e-7)
+
+
+def test_decode_special_cases():
+    """one token -> V0; equal logits (q = 0) -> mean V; a single
+    index -> that V; idx order and -1 padding do not matter; the n_fresh tail
+    is attended once even if also selected (R12)."""
+    rng = np.random.default_rng(17)
+    B, Hq, Hkv, L, D = 1, 2, 1, 40, 64
+    K, V = _kv(rng, B, Hkv, L, D), _kv(rng, B, Hkv, L, D)
+    Vf = synth.bf16_bits_to_f32(V).astype(np.float64)
+    q = synth.f32_to_bf16_bits(rng.standard_normal((B, Hq, D)).astype(np.float32))
+    one = oracle.sparse_decode(q, K, V, np.array([[[-1, 5, -1]]], np.int32), L)
+    np.testing.assert_array_equal(one[0, 0], Vf[0, 0, 5].astype(np.float32))
+    zq = np.zeros_like(q)
+    mean = oracle.sparse_decode(zq, K, V, np.array([[[1, 3, 7, 8]]], np.int32), L)
+    np.testing.assert_allclose(mean[0, 1], Vf[0, 0, [1, 3, 7, 8]].mean(axis=0), rtol=1e-6,
+                               atol=1e-7)
+    a = oracle.sparse_decode(q, K, V, np.array([[[2, 9, 30, -1]]], np.int32), L, n_fresh=1)
+    b = oracle.sparse_decode(q, K, V, np.array([[[30, -1, 9, 2]]], np.int32), L, n_fresh=1)
+    c = oracle.sparse_decode(q, K, V, np.array([[[30, 39, 9, 2]]], np.int32), L, n_fresh=1)
+    np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(a, c)
+    Kf, qf = synth.bf16_bits_to_f32(K).astype(np.float64), synth.bf16_bits_to_f32(q)
+    ref = _attn_numpy(qf[0, 0].astype(np.float64), Kf[0, 0], Vf[0, 0], [2, 9, 30, 39],
+                      1 / np.sqrt(D))
+    np.testing.assert_allclose(a[0, 0], ref, rtol=1e-6, atol=1e-7)
+
+
+# ----------------------------------------------------------------------------- generator
+def test_generator_determinism_and_sharding():
+    """§8(e): inputs are a pure function of the global index, so a shard
+    equals the matching slice of the whole tensor; two draws are identical."""
+    s = synth.base_seed(0)
+    full = synth.kv_cache(s, synth.STREAM_K, 2, 4, 33, 16)
+    part = synth.kv_cache(s, synth.STREAM_K, 2, 4, 33, 16, b0=1, h0=2, batch_slice=1,
+                          head_slice=2)
+    np.testing.assert_array_equal(full[1:2, 2:4], part)
+    w1, q1 = synth.query_trace(s, 2, 8, 16, 32)
+    w2, q2 = synth.query_trace(s, 2, 8, 16, 32, h0=4, head_slice=4)
+    np.testing.assert_array_equal(w1[:, 4:], w2)
+    np.testing.assert_array_equal(q1[:, 4:], q2)
+    x = synth.bf16_bits_to_f32(synth.kv_cache(s, synth.STREAM_V, 4, 8, 512, 128))
+    assert abs(float(x.mean())) < 0.01 and abs(float(x.std()) - 1.0) < 0.01

@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""bench.py -- AsyncSpade decode hot path on B200 (one attention layer's step).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl asyncspade|reference]
+
+Workload: BASELINE.json configs[2] -- Qwen3-32B attention shape (64 q heads /
+8 KV heads, head_dim 128), batch 64, 32k context, top-k 2048 (1/16), window 16
+-- with seeded synthetic inputs.  A step is one pass of the
+whole path: a1 predict -> a2 score -> a3 top-k -> a4 sparse decode (SURVEY
+§8(a)).  N > 1 (torchrun, one rank per GPU): KV heads are sharded over ranks
+(total work fixed -> "strong" scaling), no collective inside the step; the
+output all-gather (NCCL) is timed separately.
+
+Prints ONE JSON line (rank 0).  Timing: device CUDA events on the launching
+stream, W warm-up steps, barrier + synchronize around exactly K steps, max
+over ranks.  Inputs (K + V = 8.6 GB at N = 1) are far larger than the 126 MB
+L2, so no flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "µs/decode step (select+sparse attn) & HBM TB/s, Qwen3-32B bs64 ctx32k"
+UNIT = "us/step"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="asyncspade", choices=["asyncspade", "reference"])
+    ap.add_argument("--config", default="qwen3-32b_b64_ctx32k")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="short run for ncu: skip clocks, e2e and the CPU baseline")
+    return ap.parse_args()
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _traffic():
+    """dram bytes per launch of the dominant call, from the committed ncu
+    --set full summary (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f).get("score_select_dram_bytes_per_launch")
+    return None
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- reference arm
+def _oracle_rows(cfg, rows, seed):
+    """Host inputs for sampled (b, kv-head) rows (generation excluded from timing)."""
+    from paper_2510_07486_b200 import synth
+    G, D, L = cfg.group, cfg.head_dim, cfg.seq_len
+    data = []
+    for r in rows:
+        b, h = divmod(int(r), cfg.n_kv_heads)
+        win, q = synth.query_trace(seed, cfg.batch, cfg.n_q_heads, cfg.window, D, b0=b,
+                                   h0=h * G, batch_slice=1, head_slice=G)
+        K = synth.kv_rows(seed, synth.STREAM_K, b, h, 0, L, cfg.n_kv_heads, L, D)[None, None]
+        V = synth.kv_rows(seed, synth.STREAM_V, b, h, 0, L, cfg.n_kv_heads, L, D)[None, None]
+        data.append((win, q, K, V))
+    return data
+
+
+def _oracle_time(cfg, data):
+    """Wall time of the oracle's full step (c1 -> c2 -> c3 -> c4) over the rows."""
+    import oracle
+    t0 = time.perf_counter()
+    for win, q, K, V in data:
+        oracle.step(win, q, K, V, [cfg.seq_len], cfg.top_k)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, target_s: float = 12.0):
+    """The oracle, as it stands (one thread), on a bounded sample of rows."""
+    from paper_2510_07486_b200 import synth
+    seed = synth.base_seed(cfg.index)
+    n_rows_total = cfg.batch * cfg.n_kv_heads
+    probe = _oracle_rows(cfg, [0], seed)
+    t1 = _oracle_time(cfg, probe)
+    n = max(1, min(n_rows_total, int(target_s / max(t1, 1e-3))))
+    rows = [int(i * n_rows_total / n) for i in range(n)]
+    data = _oracle_rows(cfg, rows, seed)
+    t = _oracle_time(cfg, data)
+    us_per_step = t / n * n_rows_total * 1e6
+    return {"value": us_per_step, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{n} of {n_rows_total} (batch, kv-head) rows of {cfg.name}, full step "
+                      f"(predict, fp64 score, full sort, fp64 decode), scaled to a whole step; "
+                      f"{t:.1f} s wall"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2510_07486_b200 import synth
+    seed = synth.base_seed(cfg.index)
+    n_rows_total = cfg.batch * cfg.n_kv_heads
+    rows_per_step = 4
+    times = []
+    for i in range(args.warmup + args.steps):
+        rows = [(i * rows_per_step + j) * 37 % n_rows_total for j in range(rows_per_step)]
+        data = _oracle_rows(cfg, rows, seed)
+        t = _oracle_time(cfg, data)
+        if i >= args.warmup:
+            times.append(t / rows_per_step * n_rows_total * 1e6)
+    v = statistics.mean(times)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": v / 1e3, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "batch": cfg.batch, "n_q_heads": cfg.n_q_heads,
+                       "n_kv_heads": cfg.n_kv_heads, "head_dim": cfg.head_dim,
+                       "seq_len": cfg.seq_len, "top_k": cfg.top_k, "window": cfg.window},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{rows_per_step} of {n_rows_total} (batch, kv-head) rows "
+                                       "per step, full oracle step, scaled to a whole step"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def main():
+    args = _args()
+    from paper_2510_07486_b200 import configs
+    cfg = {c.name: c for c in (configs.TINY, configs.QWEN3_8B, configs.QWEN3_32B)}[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2510_07486_b200 as asp
+    from paper_2510_07486_b200.step import DecodeStep
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if cfg.n_kv_heads % world:
+        raise SystemExit("KV heads must divide evenly over ranks")
+    hn = cfg.n_kv_heads // world
+    step = DecodeStep(cfg, "cuda", kv_heads=(rank * hn, hn))
+    step.fill_synthetic()
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+
+    def one_step(evs=None):
+        if evs is not None:
+            evs[0].record(stream)
+        asp.predict_query(step.window, step.q_hat, dev_flags=step.dev_flags, params=step.p_pred)
+        if evs is not None:
+            evs[1].record(stream)
+        asp.score_select(step.q_hat, step.k_cache, step.seq_lens, cfg.top_k, sel_idx=step.sel_idx,
+                         workspace=step.ws_sel, dev_flags=step.dev_flags, params=step.p_sel)
+        if evs is not None:
+            evs[2].record(stream)
+        asp.sparse_decode(step.q, step.k_cache, step.v_cache, step.seq_lens, step.sel_idx,
+                          out=step.out, workspace=step.ws_dec, params=step.p_dec)
+        if evs is not None:
+            evs[3].record(stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 1)):
+        one_step()
+    barrier()
+    events = [[ev() for _ in range(4)] for _ in range(args.steps)]
+    with Clocks(local) as clk:
+        barrier()
+        for i in range(args.steps):
+            one_step(events[i])
+        barrier()
+    t_total = events[0][0].elapsed_time(events[-1][3])            # ms, device time
+    seg = [[e[j].elapsed_time(e[j + 1]) for e in events] for j in range(3)]
+    avg_pred, avg_sel, avg_dec = (statistics.mean(s) for s in seg)
+    ms_step = t_total / args.steps
+    t = torch.tensor([ms_step, avg_sel], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step, avg_sel_max = float(t[0]), float(t[1])
+    flags = int(step.dev_flags.item())
+
+    # output all-gather (NCCL) timed separately: in a TP model o_proj consumes the shard
+    gather_ms = None
+    if world > 1:
+        full = torch.empty(world, *step.out.shape, dtype=step.out.dtype, device="cuda")
+        for _ in range(3):
+            dist.all_gather_into_tensor(full, step.out)
+        barrier()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for _ in range(10):
+            dist.all_gather_into_tensor(full, step.out)
+        e1.record(stream)
+        barrier()
+        gather_ms = e0.elapsed_time(e1) / 10
+
+    # e2e through the public API with host buffers (pinned): per step H2D of
+    # the new query state q_t (window push, fp32), the current query q (bf16)
+    # and the new token's k/v rows; D2H of the attention output.
+    e2e = None
+    if not (args.no_e2e or args.profile):
+        B, nq, D = cfg.batch, step.n_q, cfg.head_dim
+        h_qt = torch.randn(B, nq, D, dtype=torch.float32).pin_memory()
+        h_q = torch.randn(B, nq, D).to(torch.bfloat16).pin_memory()
+        h_kv = torch.randn(2, B, step.n_kv, D).to(torch.bfloat16).pin_memory()
+        h_out = torch.empty(B, nq, D, dtype=torch.float32).pin_memory()
+        d_qt = torch.empty(B, nq, D, dtype=torch.float32, device="cuda")
+        L = cfg.seq_len
+
+        def e2e_step():
+            d_qt.copy_(h_qt, non_blocking=True)
+            step.push_query(d_qt)
+            step.q.copy_(h_q, non_blocking=True)
+            step.k_cache[:, :, L - 1].copy_(h_kv[0], non_blocking=True)
+            step.v_cache[:, :, L - 1].copy_(h_kv[1], non_blocking=True)
+            one_step()
+            h_out.copy_(step.out, non_blocking=True)
+
+        for _ in range(3):
+            e2e_step()
+        barrier()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        barrier()
+        tt = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        bi = h_qt.numel() * 4 + h_q.numel() * 2 + h_kv.numel() * 2
+        bo = h_out.numel() * 4
+        e2e = {"value": float(tt[0]) * 1e3, "unit": UNIT, "h2d_bytes_per_step": bi * world,
+               "d2h_bytes_per_step": bo * world}
+
+    if rank == 0:
+        peak, peak_src = _peaks()
+        core = cfg.core_bytes(hn)                      # per GPU
+        k_bytes = cfg.batch * hn * cfg.seq_len * cfg.head_dim * 2
+        achieved = k_bytes / (avg_sel_max * 1e-3) / 1e9
+        line = {
+            "metric": METRIC, "value": ms_step * 1e3, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16 KV, fp32 math (fp64 predictor)", "data": "synthetic",
+            "config": {"workload": cfg.name, "batch": cfg.batch, "n_q_heads": cfg.n_q_heads,
+                       "n_kv_heads": cfg.n_kv_heads, "head_dim": cfg.head_dim,
+                       "seq_len": cfg.seq_len, "top_k": cfg.top_k, "window": cfg.window,
+                       "parallelism": f"kv-head shard x{world}",
+                       "l2": "no flush: K+V per GPU (%.2f GB) >> 126 MB L2" %
+                             (2 * k_bytes / 1e9)},
+            "hbm_tb_per_s": core / (ms_step * 1e-3) / 1e12,
+            "core_bytes_per_gpu": core,
+            "roofline_frac_step": core / (ms_step * 1e-3) / 1e9 / peak,
+            "per_call_ms": {"predict_query": avg_pred, "score_select": avg_sel,
+                            "sparse_decode": avg_dec},
+            "roofline": {"bound": "hbm", "kernel": "asyncspade_score_select (score + select)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": _traffic(),
+                         "algorithmic_bytes_per_launch": k_bytes, "peak_source": peak_src},
+            "gpu_launches": 5 * args.steps,
+            "dev_flags": flags,
+            "clocks": clk.summary(),
+        }
+        if gather_ms is not None:
+            line["allgather_out_ms"] = gather_ms
+        if e2e is not None:
+            line["e2e"] = e2e
+        if world == 1 and not (args.no_cpu_baseline or args.profile):
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

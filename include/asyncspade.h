@@ -1,0 +1,208 @@
+/*
+ * asyncspade.h -- C ABI of the B200 (sm_100a) AsyncSpade decode hot path.
+ *
+ * AsyncSpade (arXiv 2510.07486) hides query-aware KV selection behind the
+ * decode step by PREDICTING the next query from a window of recent queries
+ * and selecting tokens with the prediction.  The hot
+ * path of one attention layer's decode step is four kernels, exposed as
+ * three entry points:
+ *
+ *   asyncspade_predict_query   a1  q_hat from the query window     (Alg.1 Steps 1-6)
+ *   asyncspade_score_select    a2  q_hat . K scores per KV head    (Alg.1 Step 7)
+ *                              a3  per-row top-k token selection  (P:191, P:267 item (2))
+ *   asyncspade_sparse_decode   a4  attention over the picked K/V
+ *
+ * ("P:<n>" = line n of the paper text, reference/PAPER.md.)
+ *
+ * Plain C types only: callers need neither CUDA nor torch headers.  Every
+ * pointer argument named "device" must be CUDA device memory (or managed);
+ * `asp_stream` is a cudaStream_t (NULL = legacy default stream).
+ *
+ * Ownership and lifetime
+ *   The caller allocates every buffer, workspace included.  The library
+ *   never allocates, frees or synchronizes; it only enqueues work on
+ *   `stream`.  Pointers must stay valid until that work completes.  Calls
+ *   are stateless and reentrant (the only internal state is a per-device
+ *   cache of the SM count) and capturable into CUDA graphs.
+ *
+ * Errors
+ *   Every call validates its arguments on the host and returns a non-zero
+ *   asp_status BEFORE enqueuing anything if they are invalid: null
+ *   pointers, non-positive sizes, n_q_heads % n_kv_heads != 0, unsupported
+ *   head_dim (64 or 128) / group size G = n_q_heads / n_kv_heads (1, 2, 4,
+ *   8) / window (1..32), misaligned pointers (16 B), strides not multiples
+ *   of 8 elements, too-small workspace.  Launch failures return
+ *   ASP_ERR_CUDA.  Numeric conditions never fail a call: they OR a bit into
+ *   the optional device word `dev_flags` and produce the defined fallback
+ *   output documented per call.
+ *
+ * Determinism
+ *   Every output row is a function of that row's inputs and the call's
+ *   sizes only -- never of the grid, the SM count, the batch size or how
+ *   the heads are sharded over GPUs -- so a KV-head shard on rank r of P
+ *   reproduces the matching slice of the P = 1 result bit for bit.
+ */
+#ifndef ASYNCSPADE_H
+#define ASYNCSPADE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ASYNCSPADE_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define ASP_API __attribute__((visibility("default")))
+#else
+#define ASP_API
+#endif
+
+typedef int32_t asp_status;
+enum {
+    ASP_OK = 0,
+    ASP_ERR_INVALID_ARGUMENT = 1, /* null pointer, bad flag, misalignment     */
+    ASP_ERR_SHAPE = 2,            /* inconsistent or out-of-range sizes        */
+    ASP_ERR_UNSUPPORTED = 3,      /* valid but not built (head_dim, G, W)      */
+    ASP_ERR_WORKSPACE = 4,        /* workspace missing or too small            */
+    ASP_ERR_CUDA = 5              /* a CUDA launch/runtime error               */
+};
+
+/* Device-side condition bits, OR-ed into *dev_flags (a device uint32). */
+enum {
+    ASP_FLAG_NONFINITE = 1u, /* non-finite window value or score seen          */
+    ASP_FLAG_NOT_PD = 2u,    /* ridge matrix not positive definite             */
+    ASP_FLAG_SHORT_ROW = 4u  /* a row had fewer than top_k tokens (padded)     */
+};
+
+/* Predictor flags (asp_predict_params.flags).  The low nibble picks the
+ * assembly; the rest are independent bits.  Defaults (0) are SURVEY §8(c)
+ * readings R2-R8: masked-shared assembly, positive sign, relative eps,
+ * single softmax. */
+enum {
+    ASP_ASSEMBLY_MASKED_SHARED = 0u, /* Alg.1 Steps 4-6, m = W    */
+    ASP_ASSEMBLY_SINGLE = 1u,        /* Eq.4 single shifted window*/
+    ASP_ASSEMBLY_PER_WINDOW = 2u,    /* Eq.5 literal, one solve per k, m = W-1 */
+    ASP_SIGN_NEGATED = 1u << 4,      /* softmax(-omega) as Alg.1 Step 3 */
+    ASP_EPS_ABSOLUTE = 1u << 5,      /* eps is absolute, not x mean diag(G0)  */
+    ASP_NORM_NONE = 1u << 6,         /* raw ridge weights (SINGLE only; tests) */
+    ASP_DOUBLE_SOFTMAX = 1u << 7     /* literal Step 3 + Step 4 double softmax */
+};
+
+enum { ASP_AGG_MAX = 0, ASP_AGG_SUM = 1 };
+
+typedef uint16_t asp_bf16; /* raw bf16 bit pattern */
+typedef void *asp_stream;  /* cudaStream_t */
+
+/* ------------------------------------------------------------------------
+ * a1  asyncspade_predict_query
+ *
+ * Predicts q_hat_{t+1} for every (b, query head) from the window of the W
+ * most recent query states (Eq. 2-5; Alg. 1 Steps
+ * 1-6).  Default (masked-shared) computation per row, in fp64:
+ *   H = window rows 0..W-2 (oldest..Q_{t-1}), y = row W-1 (= Q_t)
+ *   G0 = H H^T, beta = H y, eps_eff = eps * mean(diag G0)   (R7)
+ *   omega = (G0 + eps_eff I)^-1 beta   (Cholesky)
+ *   for j = 1..W: n_j = min(j, W-1); r_j = softmax(omega[0..n_j-1]);
+ *                 c_j = sum_i r_j[i] * window[W-n_j+i]       (R3-R6)
+ *   q_hat = (1/W) sum_j c_j, rounded once to fp32.
+ *
+ * q_window  device fp32 [batch][n_q_heads][window][head_dim]; logical slot
+ *           j (0 = oldest, window-1 = newest) is physical slot
+ *           (ring_start + j) % window.  Read only.
+ * q_hat     device fp32 [batch][n_q_heads][head_dim], written.
+ * dev_flags nullable device uint32.
+ * Numeric fallback: a non-finite window or a non-PD ridge matrix gives
+ * q_hat = the newest query (passthrough) and sets
+ * ASP_FLAG_NONFINITE / ASP_FLAG_NOT_PD.  window == 1 is a passthrough.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    int32_t batch, n_q_heads, window, head_dim, ring_start;
+    float eps;      /* relative factor (default 1e-2) unless ASP_EPS_ABSOLUTE */
+    uint32_t flags; /* ASP_ASSEMBLY_* | ASP_SIGN_NEGATED | ...                */
+} asp_predict_params;
+
+ASP_API asp_status asyncspade_predict_query(const asp_predict_params *p, const float *q_window,
+                                    float *q_hat, uint32_t *dev_flags, asp_stream stream);
+
+/* ------------------------------------------------------------------------
+ * a2+a3  asyncspade_score_select
+ *
+ * Token criticality (Alg. 1 Step 7, in the GQA layout of P:260)
+ * followed by per-row top-k (P:267 item (2)):
+ *   s[b,h,n] = max_{g<G} sum_d q_hat[b,h*G+g,d] * K[b,h,n,d]   (R10, R11)
+ *   for n < seq_lens[b]; no 1/sqrt(D), no softmax.  (ASP_AGG_SUM: sum_g.)
+ *   sel_idx[b,h,:] = the top_k tokens of row (b,h), ties to the LOWER
+ *   index (R9), written in ascending index order.
+ * Precision: fp32 products/accumulation of the exact bf16 keys against the
+ * fp32 q_hat (within ~1e-6 relative of the exact score).
+ *
+ * q_hat     device fp32 [batch][n_q_heads][head_dim].
+ * k_cache   device bf16; element (b,h,n,d) at
+ *           b*k_stride_b + h*k_stride_h + n*k_stride_t + d (d-stride 1).
+ * seq_lens  device int32 [batch], 0 <= seq_lens[b] <= max_seq_len.
+ * sel_idx   device int32 [batch][n_kv_heads][top_k], written.  A row with
+ *           seq_lens[b] < top_k holds all its tokens then -1 padding and
+ *           sets ASP_FLAG_SHORT_ROW (R13).
+ * scores    nullable device fp32 [batch][n_kv_heads][max_seq_len]: if
+ *           given, the scores are written there (debug/parity) instead of
+ *           the workspace; positions >= seq_lens[b] are unspecified.
+ * workspace device, >= asyncspade_score_select_workspace(p) bytes, any
+ *           contents; 256-B aligned.
+ * NaN scores rank below every number and set ASP_FLAG_NONFINITE (R14).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    int32_t batch, n_q_heads, n_kv_heads, head_dim, top_k, max_seq_len, aggregation;
+    int64_t k_stride_b, k_stride_h, k_stride_t; /* elements */
+} asp_select_params;
+
+ASP_API size_t asyncspade_score_select_workspace(const asp_select_params *p);
+ASP_API asp_status asyncspade_score_select(const asp_select_params *p, const float *q_hat,
+                                   const asp_bf16 *k_cache, const int32_t *seq_lens,
+                                   int32_t *sel_idx, float *scores, void *workspace,
+                                   size_t workspace_bytes, uint32_t *dev_flags,
+                                   asp_stream stream);
+
+/* ------------------------------------------------------------------------
+ * a4  asyncspade_sparse_decode
+ *
+ * Decode attention of the current query over the selected tokens only
+ * ("participate in the attention computation").  For query
+ * head hq of KV head h = hq / G, the attended set is
+ *     { sel_idx[b,h,j] : 0 <= sel_idx < seq_lens[b] - n_fresh }
+ *   U [seq_lens[b] - n_fresh, seq_lens[b])                       (R12)
+ * (each token once; -1 and out-of-range entries are ignored), and
+ *     out = sum_j softmax_j(sm_scale * q . K_j) V_j
+ * with fp32 logits (bf16 x bf16 products are exact), fp32 softmax and fp32
+ * accumulation, split over fixed 256-entry chunks of the selection merged
+ * in a fixed order.  An empty set gives out = 0.
+ *
+ * q         device bf16 [batch][n_q_heads][head_dim].
+ * k_cache, v_cache  device bf16, strided like asp_select_params' K.
+ * seq_lens  device int32 [batch].   sel_idx device int32 [batch][n_kv_heads][top_k].
+ * out       device fp32 [batch][n_q_heads][head_dim], written.
+ * workspace device, >= asyncspade_sparse_decode_workspace(p) bytes.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    int32_t batch, n_q_heads, n_kv_heads, head_dim, top_k, n_fresh;
+    float sm_scale; /* usually 1/sqrt(head_dim) */
+    int64_t k_stride_b, k_stride_h, k_stride_t, v_stride_b, v_stride_h, v_stride_t;
+} asp_decode_params;
+
+ASP_API size_t asyncspade_sparse_decode_workspace(const asp_decode_params *p);
+ASP_API asp_status asyncspade_sparse_decode(const asp_decode_params *p, const asp_bf16 *q,
+                                    const asp_bf16 *k_cache, const asp_bf16 *v_cache,
+                                    const int32_t *seq_lens, const int32_t *sel_idx, float *out,
+                                    void *workspace, size_t workspace_bytes, asp_stream stream);
+
+/* Human-readable name of a status code (static storage). */
+ASP_API const char *asyncspade_status_string(asp_status s);
+/* ASYNCSPADE_ABI_VERSION the library was built with. */
+ASP_API int32_t asyncspade_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ASYNCSPADE_H */

@@ -1,0 +1,225 @@
+"""paper_2510_07486_b200 -- B200-native AsyncSpade decode hot path.
+
+Thin Python binding of the C ABI in include/asyncspade.h (libasyncspade.so,
+sm_100a).  Functions keep the ABI's names and only marshal arguments: every
+step of the path runs in the library's CUDA kernels.  torch provides device
+memory and streams; nothing here computes.  There is no CPU fallback: if the
+library or a CUDA device is missing, calls raise.
+
+    predict_query   a1  q_hat from the query window           (Alg.1 Steps 1-6)
+    score_select    a2+a3  q_hat.K scores + per-row top-k
+    sparse_decode   a4  attention over the selected K/V
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libasyncspade.so")
+
+ABI_VERSION = 1
+ASP_OK = 0
+FLAG_NONFINITE, FLAG_NOT_PD, FLAG_SHORT_ROW = 1, 2, 4
+ASSEMBLY_MASKED_SHARED, ASSEMBLY_SINGLE, ASSEMBLY_PER_WINDOW = 0, 1, 2
+SIGN_NEGATED, EPS_ABSOLUTE, NORM_NONE, DOUBLE_SOFTMAX = 1 << 4, 1 << 5, 1 << 6, 1 << 7
+AGG_MAX, AGG_SUM = 0, 1
+
+EXPORTED_SYMBOLS = (
+    "asyncspade_predict_query", "asyncspade_score_select_workspace", "asyncspade_score_select",
+    "asyncspade_sparse_decode_workspace", "asyncspade_sparse_decode",
+    "asyncspade_status_string", "asyncspade_abi_version",
+)
+
+
+class PredictParams(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("n_q_heads", ctypes.c_int32),
+                ("window", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("ring_start", ctypes.c_int32), ("eps", ctypes.c_float),
+                ("flags", ctypes.c_uint32)]
+
+
+class SelectParams(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("n_q_heads", ctypes.c_int32),
+                ("n_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("top_k", ctypes.c_int32), ("max_seq_len", ctypes.c_int32),
+                ("aggregation", ctypes.c_int32),
+                ("k_stride_b", ctypes.c_int64), ("k_stride_h", ctypes.c_int64),
+                ("k_stride_t", ctypes.c_int64)]
+
+
+class DecodeParams(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("n_q_heads", ctypes.c_int32),
+                ("n_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("top_k", ctypes.c_int32), ("n_fresh", ctypes.c_int32),
+                ("sm_scale", ctypes.c_float),
+                ("k_stride_b", ctypes.c_int64), ("k_stride_h", ctypes.c_int64),
+                ("k_stride_t", ctypes.c_int64), ("v_stride_b", ctypes.c_int64),
+                ("v_stride_h", ctypes.c_int64), ("v_stride_t", ctypes.c_int64)]
+
+
+class AsyncSpadeError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libasyncspade.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise AsyncSpadeError(
+                f"{LIB_PATH} missing: run `python -m paper_2510_07486_b200.build` "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, sz = ctypes.c_void_p, ctypes.c_size_t
+        L.asyncspade_predict_query.argtypes = [ctypes.POINTER(PredictParams), vp, vp, vp, vp]
+        L.asyncspade_predict_query.restype = ctypes.c_int32
+        L.asyncspade_score_select_workspace.argtypes = [ctypes.POINTER(SelectParams)]
+        L.asyncspade_score_select_workspace.restype = sz
+        L.asyncspade_score_select.argtypes = [ctypes.POINTER(SelectParams), vp, vp, vp, vp, vp,
+                                              vp, sz, vp, vp]
+        L.asyncspade_score_select.restype = ctypes.c_int32
+        L.asyncspade_sparse_decode_workspace.argtypes = [ctypes.POINTER(DecodeParams)]
+        L.asyncspade_sparse_decode_workspace.restype = sz
+        L.asyncspade_sparse_decode.argtypes = [ctypes.POINTER(DecodeParams), vp, vp, vp, vp, vp,
+                                               vp, vp, sz, vp]
+        L.asyncspade_sparse_decode.restype = ctypes.c_int32
+        L.asyncspade_status_string.argtypes = [ctypes.c_int32]
+        L.asyncspade_status_string.restype = ctypes.c_char_p
+        L.asyncspade_abi_version.argtypes = []
+        L.asyncspade_abi_version.restype = ctypes.c_int32
+        if L.asyncspade_abi_version() != ABI_VERSION:
+            raise AsyncSpadeError("libasyncspade ABI version mismatch")
+        _lib = L
+    return _lib
+
+
+def status_string(code: int) -> str:
+    return lib().asyncspade_status_string(code).decode()
+
+
+def _check(code: int, what: str) -> None:
+    if code != ASP_OK:
+        raise AsyncSpadeError(f"{what}: {status_string(code)} ({code})")
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _u16(t: torch.Tensor) -> torch.Tensor:
+    """bf16 tensors are passed as their raw bit pattern."""
+    return t if t.dtype != torch.bfloat16 else t.view(torch.int16)
+
+
+# --------------------------------------------------------------------------- params
+def predict_params(q_window: torch.Tensor, eps=1e-2, flags=0, ring_start=0) -> PredictParams:
+    B, Hq, W, D = q_window.shape
+    return PredictParams(B, Hq, W, D, ring_start, eps, flags)
+
+
+def select_params(q_hat: torch.Tensor, k_cache: torch.Tensor, top_k: int,
+                  aggregation: int = AGG_MAX) -> SelectParams:
+    B, Hq, D = q_hat.shape
+    _, Hkv, L, _ = k_cache.shape
+    sb, sh, st, sd = k_cache.stride()
+    if sd != 1:
+        raise AsyncSpadeError("k_cache must have unit stride along head_dim")
+    return SelectParams(B, Hq, Hkv, D, top_k, L, aggregation, sb, sh, st)
+
+
+def decode_params(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, top_k: int,
+                  n_fresh: int = 0, sm_scale: float | None = None) -> DecodeParams:
+    B, Hq, D = q.shape
+    _, Hkv, _, _ = k_cache.shape
+    if k_cache.stride(3) != 1 or v_cache.stride(3) != 1:
+        raise AsyncSpadeError("caches must have unit stride along head_dim")
+    if sm_scale is None:
+        sm_scale = D ** -0.5
+    return DecodeParams(B, Hq, Hkv, D, top_k, n_fresh, sm_scale, *k_cache.stride()[:3],
+                        *v_cache.stride()[:3])
+
+
+def score_select_workspace(p: SelectParams) -> int:
+    return int(lib().asyncspade_score_select_workspace(ctypes.byref(p)))
+
+
+def sparse_decode_workspace(p: DecodeParams) -> int:
+    return int(lib().asyncspade_sparse_decode_workspace(ctypes.byref(p)))
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+
+
+# --------------------------------------------------------------------------- entry points
+def predict_query(q_window: torch.Tensor, q_hat: torch.Tensor | None = None, *, eps: float = 1e-2,
+                  flags: int = 0, ring_start: int = 0, dev_flags: torch.Tensor | None = None,
+                  stream=None, params: PredictParams | None = None) -> torch.Tensor:
+    """a1 -> asyncspade_predict_query.  q_window fp32 [B, Hq, W, D] (ring
+    order per ring_start); returns q_hat fp32 [B, Hq, D]."""
+    p = params or predict_params(q_window, eps, flags, ring_start)
+    if q_hat is None:
+        q_hat = torch.empty(q_window.shape[0], q_window.shape[1], q_window.shape[3],
+                            dtype=torch.float32, device=q_window.device)
+    _check(lib().asyncspade_predict_query(ctypes.byref(p), _ptr(q_window), _ptr(q_hat),
+                                          _ptr(dev_flags), _stream(stream)),
+           "asyncspade_predict_query")
+    return q_hat
+
+
+def score_select(q_hat: torch.Tensor, k_cache: torch.Tensor, seq_lens: torch.Tensor, top_k: int,
+                 *, sel_idx: torch.Tensor | None = None, scores: torch.Tensor | None = None,
+                 workspace: torch.Tensor | None = None, aggregation: int = AGG_MAX,
+                 dev_flags: torch.Tensor | None = None, stream=None,
+                 params: SelectParams | None = None) -> torch.Tensor:
+    """a2+a3 -> asyncspade_score_select.  q_hat fp32 [B, Hq, D]; k_cache bf16
+    [B, Hkv, L, D] (strided, unit d-stride); seq_lens int32 [B].  Returns
+    sel_idx int32 [B, Hkv, top_k] (ascending, -1 padded)."""
+    p = params or select_params(q_hat, k_cache, top_k, aggregation)
+    if sel_idx is None:
+        sel_idx = torch.empty(p.batch, p.n_kv_heads, top_k, dtype=torch.int32,
+                              device=q_hat.device)
+    ws_bytes = 0
+    if scores is None:
+        ws_bytes = score_select_workspace(p)
+        if workspace is None:
+            workspace = _workspace(ws_bytes, q_hat.device)
+        ws_bytes = workspace.numel() * workspace.element_size()
+    _check(lib().asyncspade_score_select(ctypes.byref(p), _ptr(q_hat), _ptr(_u16(k_cache)),
+                                         _ptr(seq_lens), _ptr(sel_idx), _ptr(scores),
+                                         _ptr(workspace), ws_bytes, _ptr(dev_flags),
+                                         _stream(stream)),
+           "asyncspade_score_select")
+    return sel_idx
+
+
+def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
+                  seq_lens: torch.Tensor, sel_idx: torch.Tensor, *, n_fresh: int = 0,
+                  sm_scale: float | None = None, out: torch.Tensor | None = None,
+                  workspace: torch.Tensor | None = None, stream=None,
+                  params: DecodeParams | None = None) -> torch.Tensor:
+    """a4 -> asyncspade_sparse_decode.  q bf16 [B, Hq, D]; caches bf16
+    [B, Hkv, L, D]; sel_idx int32 [B, Hkv, k].  Returns out fp32 [B, Hq, D]."""
+    p = params or decode_params(q, k_cache, v_cache, sel_idx.shape[-1], n_fresh, sm_scale)
+    if out is None:
+        out = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+    if workspace is None:
+        workspace = _workspace(sparse_decode_workspace(p), q.device)
+    ws_bytes = workspace.numel() * workspace.element_size()
+    _check(lib().asyncspade_sparse_decode(ctypes.byref(p), _ptr(_u16(q)), _ptr(_u16(k_cache)),
+                                          _ptr(_u16(v_cache)), _ptr(seq_lens), _ptr(sel_idx),
+                                          _ptr(out), _ptr(workspace), ws_bytes, _stream(stream)),
+           "asyncspade_sparse_decode")
+    return out

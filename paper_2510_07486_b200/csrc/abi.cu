@@ -1,0 +1,142 @@
+// abi.cu -- the extern "C" boundary (include/asyncspade.h): host-side
+// validation, workspace sizing, and the launches.  Nothing is enqueued unless
+// every check passes.
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace {
+
+bool aligned16(const void *ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
+bool group_ok(int G) { return G == 1 || G == 2 || G == 4 || G == 8; }
+bool dim_ok(int D) { return D == 64 || D == 128; }
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+asp_status from_cuda(cudaError_t e) { return e == cudaSuccess ? ASP_OK : ASP_ERR_CUDA; }
+
+asp_status check_select(const asp_select_params *p) {
+    if (!p) return ASP_ERR_INVALID_ARGUMENT;
+    if (p->batch <= 0 || p->n_q_heads <= 0 || p->n_kv_heads <= 0 || p->head_dim <= 0 ||
+        p->top_k <= 0 || p->max_seq_len <= 0)
+        return ASP_ERR_SHAPE;
+    if (p->n_q_heads % p->n_kv_heads) return ASP_ERR_SHAPE;
+    if (!dim_ok(p->head_dim) || !group_ok(p->n_q_heads / p->n_kv_heads)) return ASP_ERR_UNSUPPORTED;
+    if (p->aggregation != ASP_AGG_MAX && p->aggregation != ASP_AGG_SUM) return ASP_ERR_INVALID_ARGUMENT;
+    if (p->k_stride_t < p->head_dim || p->k_stride_b < 0 || p->k_stride_h < 0) return ASP_ERR_SHAPE;
+    if ((p->k_stride_b | p->k_stride_h | p->k_stride_t) & 7) return ASP_ERR_INVALID_ARGUMENT;
+    return ASP_OK;
+}
+
+asp_status check_decode(const asp_decode_params *p) {
+    if (!p) return ASP_ERR_INVALID_ARGUMENT;
+    if (p->batch <= 0 || p->n_q_heads <= 0 || p->n_kv_heads <= 0 || p->head_dim <= 0 ||
+        p->top_k <= 0 || p->n_fresh < 0)
+        return ASP_ERR_SHAPE;
+    if (p->n_q_heads % p->n_kv_heads) return ASP_ERR_SHAPE;
+    if (!dim_ok(p->head_dim) || !group_ok(p->n_q_heads / p->n_kv_heads)) return ASP_ERR_UNSUPPORTED;
+    if (!(p->sm_scale == p->sm_scale)) return ASP_ERR_INVALID_ARGUMENT;
+    if (p->k_stride_t < p->head_dim || p->v_stride_t < p->head_dim || p->k_stride_b < 0 ||
+        p->k_stride_h < 0 || p->v_stride_b < 0 || p->v_stride_h < 0)
+        return ASP_ERR_SHAPE;
+    if ((p->k_stride_b | p->k_stride_h | p->k_stride_t | p->v_stride_b | p->v_stride_h |
+         p->v_stride_t) & 7)
+        return ASP_ERR_INVALID_ARGUMENT;
+    return ASP_OK;
+}
+
+}  // namespace
+
+int asp_sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 148;
+    if (!cached[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = n > 0 ? n : 148;
+    }
+    return cached[dev];
+}
+
+extern "C" {
+
+asp_status asyncspade_predict_query(const asp_predict_params *p, const float *q_window,
+                                    float *q_hat, uint32_t *dev_flags, asp_stream stream) {
+    if (!p || !q_window || !q_hat) return ASP_ERR_INVALID_ARGUMENT;
+    if (p->batch <= 0 || p->n_q_heads <= 0 || p->head_dim <= 0 || p->window <= 0)
+        return ASP_ERR_SHAPE;
+    if (p->ring_start < 0 || p->ring_start >= p->window) return ASP_ERR_SHAPE;
+    if (!dim_ok(p->head_dim) || p->window > 32) return ASP_ERR_UNSUPPORTED;
+    const uint32_t mode = p->flags & 0xFu;
+    const uint32_t known = 0xFu | ASP_SIGN_NEGATED | ASP_EPS_ABSOLUTE | ASP_NORM_NONE |
+                           ASP_DOUBLE_SOFTMAX;
+    if (mode > ASP_ASSEMBLY_PER_WINDOW || (p->flags & ~known)) return ASP_ERR_INVALID_ARGUMENT;
+    if ((p->flags & ASP_NORM_NONE) && mode != ASP_ASSEMBLY_SINGLE) return ASP_ERR_INVALID_ARGUMENT;
+    if (!(p->eps == p->eps)) return ASP_ERR_INVALID_ARGUMENT;
+    if (!aligned16(q_window) || !aligned16(q_hat)) return ASP_ERR_INVALID_ARGUMENT;
+    return from_cuda(asp_launch_predict(*p, q_window, q_hat, dev_flags, (cudaStream_t)stream));
+}
+
+size_t asyncspade_score_select_workspace(const asp_select_params *p) {
+    if (check_select(p) != ASP_OK) return 0;
+    return align256((size_t)p->batch * p->n_kv_heads * p->max_seq_len * sizeof(float));
+}
+
+asp_status asyncspade_score_select(const asp_select_params *p, const float *q_hat,
+                                   const asp_bf16 *k_cache, const int32_t *seq_lens,
+                                   int32_t *sel_idx, float *scores, void *workspace,
+                                   size_t workspace_bytes, uint32_t *dev_flags,
+                                   asp_stream stream) {
+    asp_status st = check_select(p);
+    if (st != ASP_OK) return st;
+    if (!q_hat || !k_cache || !seq_lens || !sel_idx) return ASP_ERR_INVALID_ARGUMENT;
+    if (!aligned16(q_hat) || !aligned16(k_cache) || !aligned16(scores)) return ASP_ERR_INVALID_ARGUMENT;
+    float *s_buf = scores;
+    if (!s_buf) {
+        if (!workspace || workspace_bytes < asyncspade_score_select_workspace(p))
+            return ASP_ERR_WORKSPACE;
+        if (reinterpret_cast<uintptr_t>(workspace) & 255u) return ASP_ERR_WORKSPACE;
+        s_buf = static_cast<float *>(workspace);
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = asp_launch_score(*p, q_hat, k_cache, seq_lens, s_buf, dev_flags, s);
+    if (e != cudaSuccess) return ASP_ERR_CUDA;
+    return from_cuda(asp_launch_select(*p, s_buf, seq_lens, sel_idx, dev_flags, s));
+}
+
+size_t asyncspade_sparse_decode_workspace(const asp_decode_params *p) {
+    if (check_decode(p) != ASP_OK) return 0;
+    return align256(asp_decode_partials_bytes(*p));
+}
+
+asp_status asyncspade_sparse_decode(const asp_decode_params *p, const asp_bf16 *q,
+                                    const asp_bf16 *k_cache, const asp_bf16 *v_cache,
+                                    const int32_t *seq_lens, const int32_t *sel_idx, float *out,
+                                    void *workspace, size_t workspace_bytes, asp_stream stream) {
+    asp_status st = check_decode(p);
+    if (st != ASP_OK) return st;
+    if (!q || !k_cache || !v_cache || !seq_lens || !sel_idx || !out) return ASP_ERR_INVALID_ARGUMENT;
+    if (!aligned16(q) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out))
+        return ASP_ERR_INVALID_ARGUMENT;
+    if (!workspace || workspace_bytes < asyncspade_sparse_decode_workspace(p)) return ASP_ERR_WORKSPACE;
+    if (reinterpret_cast<uintptr_t>(workspace) & 255u) return ASP_ERR_WORKSPACE;
+    return from_cuda(asp_launch_decode(*p, q, k_cache, v_cache, seq_lens, sel_idx, out,
+                                       static_cast<float *>(workspace), (cudaStream_t)stream));
+}
+
+const char *asyncspade_status_string(asp_status s) {
+    switch (s) {
+        case ASP_OK: return "ASP_OK";
+        case ASP_ERR_INVALID_ARGUMENT: return "ASP_ERR_INVALID_ARGUMENT";
+        case ASP_ERR_SHAPE: return "ASP_ERR_SHAPE";
+        case ASP_ERR_UNSUPPORTED: return "ASP_ERR_UNSUPPORTED";
+        case ASP_ERR_WORKSPACE: return "ASP_ERR_WORKSPACE";
+        case ASP_ERR_CUDA: return "ASP_ERR_CUDA";
+        default: return "ASP_ERR_UNKNOWN";
+    }
+}
+
+int32_t asyncspade_abi_version(void) { return ASYNCSPADE_ABI_VERSION; }
+
+}  // extern "C"

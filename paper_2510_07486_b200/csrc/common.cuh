@@ -1,0 +1,72 @@
+// common.cuh -- small device helpers shared by the sm_100a kernels of the
+// product path.  (Nothing here is shared with oracle/.)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "asyncspade.h"
+
+#define ASP_DEV __device__ __forceinline__
+
+namespace asp {
+
+// bf16 pair packed in a 32-bit word -> two fp32 (exact: a bf16 is the top
+// half of an fp32).
+ASP_DEV float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+ASP_DEV float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+ASP_DEV float bf16f(uint16_t h) { return __uint_as_float(((uint32_t)h) << 16); }
+
+ASP_DEV float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+ASP_DEV float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Order-preserving map fp32 score -> uint32 key (larger score, larger key).
+// -0.0 is canonicalised to +0.0 (they tie); NaN maps to 0, below every
+// number including -inf (reading R14).
+ASP_DEV uint32_t score_key(float f) {
+    if (f != f) return 0u;
+    if (f == 0.0f) f = 0.0f;
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+ASP_DEV void flag_or(uint32_t *dev_flags, uint32_t bits) {
+    if (dev_flags && bits) atomicOr(dev_flags, bits);
+}
+
+// 2xfp32 packed FMA (Blackwell FFMA2): d = a * b + c on both halves.
+ASP_DEV float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(*reinterpret_cast<unsigned long long *>(&d))
+        : "l"(*reinterpret_cast<unsigned long long *>(&a)),
+          "l"(*reinterpret_cast<unsigned long long *>(&b)),
+          "l"(*reinterpret_cast<unsigned long long *>(&c)));
+    return d;
+}
+
+}  // namespace asp
+
+// Internal launchers (implemented per kernel file, called by abi.cu after
+// host-side validation).  They return cudaGetLastError() of the launch.
+cudaError_t asp_launch_predict(const asp_predict_params &p, const float *q_window, float *q_hat,
+                               uint32_t *dev_flags, cudaStream_t s);
+cudaError_t asp_launch_score(const asp_select_params &p, const float *q_hat,
+                             const asp_bf16 *k_cache, const int32_t *seq_lens, float *scores,
+                             uint32_t *dev_flags, cudaStream_t s);
+cudaError_t asp_launch_select(const asp_select_params &p, const float *scores,
+                              const int32_t *seq_lens, int32_t *sel_idx, uint32_t *dev_flags,
+                              cudaStream_t s);
+size_t asp_decode_partials_bytes(const asp_decode_params &p);
+cudaError_t asp_launch_decode(const asp_decode_params &p, const asp_bf16 *q,
+                              const asp_bf16 *k_cache, const asp_bf16 *v_cache,
+                              const int32_t *seq_lens, const int32_t *sel_idx, float *out,
+                              float *partials, cudaStream_t s);
+int asp_sm_count();

@@ -1,0 +1,89 @@
+// synth.cu -- device-side seeded input generator (bench/test support, NOT part
+// of the product ABI; built into libasp_synth.so).  Bit-for-bit the same
+// definition as paper_2510_07486_b200/synth.py: splitmix64 counter hash ->
+// Irwin-Hall(4) normal deviate (integer sum, one RN fp32 multiply) -> RNE
+// bf16; AR(1) query traces q_t = 0.95 q_{t-1} + 0.05 xi_t
+// with separately rounded fp32 multiplies and add.  Holds none of the
+// method's arithmetic.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace {
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ float normal_at(uint64_t key, uint64_t idx) {
+    const uint64_t z = splitmix64(key + idx);
+    const int64_t s = (int64_t)((z & 0xFFFF) + ((z >> 16) & 0xFFFF) + ((z >> 32) & 0xFFFF) +
+                                (z >> 48)) - 131070;
+    return __fmul_rn((float)s, __uint_as_float(0x37ddb3d7u));  // fp32(1/37837.22668)
+}
+
+__device__ __forceinline__ uint16_t bf16_rne(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return (uint16_t)((b + 0x7FFFu + ((b >> 16) & 1u)) >> 16);
+}
+
+__global__ void kv_kernel(uint64_t key, uint16_t *dst, int bs, int hs, int L, int D, int b0, int h0,
+                          int hg, long long sb, long long sh, long long st) {
+    const long long total = (long long)bs * hs * L * D;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int d = (int)(e % D);
+        long long r = e / D;
+        const int t = (int)(r % L);
+        r /= L;
+        const int h = (int)(r % hs);
+        const int b = (int)(r / hs);
+        const uint64_t idx =
+            (((uint64_t)(b0 + b) * (uint64_t)hg + (uint64_t)(h0 + h)) * (uint64_t)L + (uint64_t)t) *
+                (uint64_t)D + (uint64_t)d;
+        dst[b * sb + h * sh + (long long)t * st + d] = bf16_rne(normal_at(key, idx));
+    }
+}
+
+__global__ void query_kernel(uint64_t key, float *window, uint16_t *q, int bs, int hs, int W,
+                             int D, int b0, int h0, int hg) {
+    const long long total = (long long)bs * hs * D;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int d = (int)(e % D);
+        const long long r = e / D;
+        const int h = (int)(r % hs);
+        const int b = (int)(r / hs);
+        const int T = W + 1;
+        const uint64_t rowbase = ((uint64_t)(b0 + b) * (uint64_t)hg + (uint64_t)(h0 + h)) * (uint64_t)T;
+        float v = 0.0f;
+        for (int t = 0; t < T; t++) {
+            const float xi = normal_at(key, (rowbase + (uint64_t)t) * (uint64_t)D + (uint64_t)d);
+            v = (t == 0) ? xi : __fadd_rn(__fmul_rn(0.95f, v), __fmul_rn(0.05f, xi));
+            if (t < W) window[((r * W) + t) * D + d] = v;
+            else q[r * D + d] = bf16_rne(v);
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int asp_synth_kv(uint64_t stream_key, uint16_t *dst, int bs, int hs, int L, int D, int b0, int h0,
+                 int hg, long long sb, long long sh, long long st, void *stream) {
+    kv_kernel<<<4096, 256, 0, (cudaStream_t)stream>>>(stream_key, dst, bs, hs, L, D, b0, h0, hg,
+                                                      sb, sh, st);
+    return (int)cudaGetLastError();
+}
+
+int asp_synth_query(uint64_t stream_key, float *window, uint16_t *q, int bs, int hs, int W, int D,
+                    int b0, int h0, int hg, void *stream) {
+    query_kernel<<<1024, 256, 0, (cudaStream_t)stream>>>(stream_key, window, q, bs, hs, W, D, b0,
+                                                         h0, hg);
+    return (int)cudaGetLastError();
+}
+
+}  // extern "C"

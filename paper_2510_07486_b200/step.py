@@ -1,0 +1,105 @@
+"""DecodeStep -- one attention layer's AsyncSpade decode step on one GPU.
+
+The public "whole path" API: it owns the device buffers of one (possibly
+KV-head-sharded) layer and runs a1 -> a2+a3 -> a4 through the C ABI
+(predict_query, score_select, sparse_decode), optionally replayed as a CUDA
+graph.  torch is used only to allocate memory and provide the stream.
+
+Sharding (§8(e) of SURVEY.md): a shard owns KV heads
+[h0, h0 + n_kv_heads) and the matching q heads for every batch row.  Every
+kernel's per-row arithmetic depends only on the row, so a shard reproduces
+the matching slice of the unsharded result bit for bit.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import (decode_params, predict_params, predict_query, score_select, select_params,
+               sparse_decode, score_select_workspace, sparse_decode_workspace)
+from . import synth
+from .configs import Config
+
+
+class DecodeStep:
+    def __init__(self, cfg: Config, device="cuda", *, kv_heads: tuple[int, int] | None = None,
+                 n_fresh: int = 0, eps: float = 1e-2, flags: int = 0, keep_scores: bool = False):
+        self.cfg = cfg
+        self.device = torch.device(device)
+        h0, hn = kv_heads if kv_heads is not None else (0, cfg.n_kv_heads)
+        self.h0, self.n_kv = h0, hn
+        G = cfg.group
+        self.q0, self.n_q = h0 * G, hn * G
+        B, W, D, L = cfg.batch, cfg.window, cfg.head_dim, cfg.seq_len
+        dev = self.device
+        self.n_fresh, self.eps, self.flags = n_fresh, eps, flags
+        self.ring_start = 0
+        self.window = torch.empty(B, self.n_q, W, D, dtype=torch.float32, device=dev)
+        self.q = torch.empty(B, self.n_q, D, dtype=torch.bfloat16, device=dev)
+        self.k_cache = torch.empty(B, hn, L, D, dtype=torch.bfloat16, device=dev)
+        self.v_cache = torch.empty(B, hn, L, D, dtype=torch.bfloat16, device=dev)
+        self.seq_lens = torch.full((B,), L, dtype=torch.int32, device=dev)
+        self.q_hat = torch.empty(B, self.n_q, D, dtype=torch.float32, device=dev)
+        self.sel_idx = torch.empty(B, hn, cfg.top_k, dtype=torch.int32, device=dev)
+        self.out = torch.empty(B, self.n_q, D, dtype=torch.float32, device=dev)
+        self.dev_flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.scores = (torch.empty(B, hn, L, dtype=torch.float32, device=dev)
+                       if keep_scores else None)
+        self.p_pred = predict_params(self.window, eps, flags, 0)
+        self.p_sel = select_params(self.q_hat, self.k_cache, cfg.top_k)
+        self.p_dec = decode_params(self.q, self.k_cache, self.v_cache, cfg.top_k, n_fresh)
+        self.ws_sel = torch.empty(max(score_select_workspace(self.p_sel), 256), dtype=torch.uint8,
+                                  device=dev)
+        self.ws_dec = torch.empty(max(sparse_decode_workspace(self.p_dec), 256),
+                                  dtype=torch.uint8, device=dev)
+        self.graph = None
+
+    # ------------------------------------------------------------------ inputs
+    def fill_synthetic(self, seed: int | None = None) -> None:
+        """Seeded synthetic inputs of the config's shape: the
+        values of global heads [h0, h0+n) -- identical on any sharding."""
+        cfg = self.cfg
+        seed = synth.base_seed(cfg.index) if seed is None else seed
+        synth.fill_kv_device(self.k_cache, seed, synth.STREAM_K, 0, self.h0, cfg.n_kv_heads)
+        synth.fill_kv_device(self.v_cache, seed, synth.STREAM_V, 0, self.h0, cfg.n_kv_heads)
+        synth.fill_query_device(self.window, self.q.view(torch.int16), seed, 0, self.q0,
+                                cfg.n_q_heads)
+        self.ring_start = 0
+        self.p_pred.ring_start = 0
+
+    # ------------------------------------------------------------------ the path
+    def run(self, stream=None) -> None:
+        """a1 -> a2+a3 -> a4 on `stream` (default: current)."""
+        predict_query(self.window, self.q_hat, dev_flags=self.dev_flags.view(torch.int32),
+                      stream=stream, params=self.p_pred)
+        score_select(self.q_hat, self.k_cache, self.seq_lens, self.cfg.top_k,
+                     sel_idx=self.sel_idx, scores=self.scores, workspace=self.ws_sel,
+                     dev_flags=self.dev_flags, stream=stream, params=self.p_sel)
+        sparse_decode(self.q, self.k_cache, self.v_cache, self.seq_lens, self.sel_idx,
+                      out=self.out, workspace=self.ws_dec, stream=stream, params=self.p_dec)
+
+    def capture(self) -> torch.cuda.CUDAGraph:
+        """Record run() once into a CUDA graph (warm-up launch first)."""
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.run()
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.run()
+        self.graph = g
+        return g
+
+    def replay(self) -> None:
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+
+    # ------------------------------------------------------------------ a0: window push
+    def push_query(self, q_t: torch.Tensor) -> None:
+        """Enqueue q_t (fp32 [B, n_q, D]) as the newest window entry, evicting
+        the oldest ("enqueues the query state to the sliding window")."""
+        slot = self.ring_start
+        self.window[:, :, slot].copy_(q_t, non_blocking=True)
+        self.ring_start = (slot + 1) % self.cfg.window
+        self.p_pred.ring_start = self.ring_start

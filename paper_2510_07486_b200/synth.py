@@ -124,3 +124,57 @@ def query_trace(seed: int, batch: int, n_q_heads: int, window: int, head_dim: in
         e = (AR_SIGMA * xi[:, :, s]).astype(np.float32)
         qs[:, :, s] = (a + e).astype(np.float32)
     return np.ascontiguousarray(qs[:, :, :window]), f32_to_bf16_bits(qs[:, :, window])
+
+
+# --------------------------------------------------------------------------- device side
+_synth_lib = None
+
+
+def _dev_lib():
+    """libasp_synth.so: the same generator as a CUDA kernel (bench/test support)."""
+    global _synth_lib
+    if _synth_lib is None:
+        import ctypes
+        import os
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libasp_synth.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run `python -m paper_2510_07486_b200.build`")
+        L = ctypes.CDLL(path)
+        i, ll, u64, vp = ctypes.c_int, ctypes.c_longlong, ctypes.c_uint64, ctypes.c_void_p
+        L.asp_synth_kv.argtypes = [u64, vp, i, i, i, i, i, i, i, ll, ll, ll, vp]
+        L.asp_synth_kv.restype = i
+        L.asp_synth_query.argtypes = [u64, vp, vp, i, i, i, i, i, i, i, vp]
+        L.asp_synth_query.restype = i
+        _synth_lib = L
+    return _synth_lib
+
+
+def fill_kv_device(cache, seed: int, stream_id: int, b0: int = 0, h0: int = 0,
+                   n_kv_heads_global: int | None = None, stream=None) -> None:
+    """Fill a bf16 torch cache view [B_s, H_s, L, D] (unit d-stride) on the GPU
+    with kv_cache(...) values; L is the view's token extent."""
+    import torch
+    bs, hs, L, D = cache.shape
+    hg = hs if n_kv_heads_global is None else n_kv_heads_global
+    st = stream if stream is not None else torch.cuda.current_stream()
+    sb, sh, stt, sd = cache.stride()
+    assert sd == 1
+    rc = _dev_lib().asp_synth_kv(stream_key(seed, stream_id), cache.data_ptr(), bs, hs, L, D,
+                                 b0, h0, hg, sb, sh, stt, st.cuda_stream)
+    if rc != 0:
+        raise RuntimeError(f"asp_synth_kv failed: cuda error {rc}")
+
+
+def fill_query_device(window, q, seed: int, b0: int = 0, h0: int = 0,
+                      n_q_heads_global: int | None = None, stream=None) -> None:
+    """Fill window fp32 [B_s, H_s, W, D] and q bf16 [B_s, H_s, D] (contiguous)
+    with query_trace(...) values on the GPU."""
+    import torch
+    bs, hs, W, D = window.shape
+    assert window.is_contiguous() and q.is_contiguous()
+    hg = hs if n_q_heads_global is None else n_q_heads_global
+    st = stream if stream is not None else torch.cuda.current_stream()
+    rc = _dev_lib().asp_synth_query(stream_key(seed, STREAM_Q), window.data_ptr(), q.data_ptr(),
+                                    bs, hs, W, D, b0, h0, hg, st.cuda_stream)
+    if rc != 0:
+        raise RuntimeError(f"asp_synth_query failed: cuda error {rc}")

@@ -1,0 +1,124 @@
+"""Host-side checks of the C-ABI library (no GPU needed): it loads, exports
+every symbol include/asyncspade.h declares, and rejects invalid arguments
+synchronously -- before anything could be enqueued."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2510_07486_b200 as asp
+from paper_2510_07486_b200 import build as asp_build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "asyncspade.h")
+
+
+@pytest.fixture(scope="module")
+def L():
+    asp_build.build()
+    return asp.lib()
+
+
+def _declared_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(asyncspade_\w+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(L):
+    names = _declared_symbols()
+    assert set(names) == set(asp.EXPORTED_SYMBOLS)
+    for n in names:
+        assert hasattr(L, n), n
+    # and nothing else leaks out of the library
+    out = os.popen(f"nm -D --defined-only {asp.LIB_PATH}").read()
+    exported = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+    assert exported == set(names)
+
+
+def test_version_and_status_strings(L):
+    assert L.asyncspade_abi_version() == asp.ABI_VERSION
+    for code, name in enumerate(["ASP_OK", "ASP_ERR_INVALID_ARGUMENT", "ASP_ERR_SHAPE",
+                                 "ASP_ERR_UNSUPPORTED", "ASP_ERR_WORKSPACE", "ASP_ERR_CUDA"]):
+        assert asp.status_string(code) == name
+    assert asp.status_string(99) == "ASP_ERR_UNKNOWN"
+
+
+FAKE = 0x10000  # 16-B aligned non-null "device" pointer: never dereferenced on error paths
+
+
+def test_predict_validation(L):
+    good = asp.PredictParams(2, 4, 16, 128, 0, 1e-2, 0)
+
+    def call(p, win=FAKE, out=FAKE):
+        return L.asyncspade_predict_query(ctypes.byref(p), win, out, None, None)
+
+    assert call(good, win=None) == 1
+    assert call(good, out=FAKE + 4) == 1                       # misaligned
+    for bad in [asp.PredictParams(0, 4, 16, 128, 0, 1e-2, 0),
+                asp.PredictParams(2, 4, 0, 128, 0, 1e-2, 0),
+                asp.PredictParams(2, 4, 16, 128, 16, 1e-2, 0)]:  # ring_start out of range
+        assert call(bad) == 2
+    assert call(asp.PredictParams(2, 4, 16, 96, 0, 1e-2, 0)) == 3   # head_dim
+    assert call(asp.PredictParams(2, 4, 33, 128, 0, 1e-2, 0)) == 3  # window
+    assert call(asp.PredictParams(2, 4, 16, 128, 0, 1e-2, 3)) == 1  # unknown assembly
+    assert call(asp.PredictParams(2, 4, 16, 128, 0, 1e-2, 1 << 9)) == 1
+    assert call(asp.PredictParams(2, 4, 16, 128, 0, 1e-2, asp.NORM_NONE)) == 1  # needs SINGLE
+    assert call(asp.PredictParams(2, 4, 16, 128, 0, float("nan"), 0)) == 1
+
+
+def _sel(**kw):
+    d = dict(batch=2, n_q_heads=32, n_kv_heads=8, head_dim=128, top_k=64, max_seq_len=1024,
+             aggregation=0, k_stride_b=8 * 1024 * 128, k_stride_h=1024 * 128, k_stride_t=128)
+    d.update(kw)
+    return asp.SelectParams(*[d[f] for f, _ in asp.SelectParams._fields_])
+
+
+def test_score_select_validation_and_workspace(L):
+    def call(p, ws=FAKE, nbytes=1 << 40, q=FAKE, k=FAKE, sl=FAKE, idx=FAKE, scores=None):
+        return L.asyncspade_score_select(ctypes.byref(p), q, k, sl, idx, scores, ws, nbytes,
+                                         None, None)
+
+    p = _sel()
+    need = L.asyncspade_score_select_workspace(ctypes.byref(p))
+    assert need >= 2 * 8 * 1024 * 4 and need % 256 == 0
+    assert call(p, q=None) == 1
+    assert call(p, k=FAKE + 2) == 1
+    assert call(p, nbytes=need - 1) == 4
+    assert call(p, ws=None) == 4
+    assert call(p, ws=FAKE + 16) == 4                          # workspace must be 256-B aligned
+    assert call(_sel(n_q_heads=30)) == 2
+    assert call(_sel(top_k=0)) == 2
+    assert call(_sel(n_q_heads=128)) == 3                      # G = 16
+    assert call(_sel(head_dim=256, k_stride_t=256)) == 3
+    assert call(_sel(aggregation=2)) == 1
+    assert call(_sel(k_stride_t=100)) == 2                     # shorter than a row
+    assert call(_sel(k_stride_t=132)) == 1                     # not a multiple of 8 elements
+    assert L.asyncspade_score_select_workspace(ctypes.byref(_sel(batch=0))) == 0
+
+
+def _dec(**kw):
+    d = dict(batch=2, n_q_heads=32, n_kv_heads=8, head_dim=128, top_k=64, n_fresh=1,
+             sm_scale=128 ** -0.5, k_stride_b=8 * 1024 * 128, k_stride_h=1024 * 128,
+             k_stride_t=128, v_stride_b=8 * 1024 * 128, v_stride_h=1024 * 128, v_stride_t=128)
+    d.update(kw)
+    return asp.DecodeParams(*[d[f] for f, _ in asp.DecodeParams._fields_])
+
+
+def test_sparse_decode_validation_and_workspace(L):
+    def call(p, ws=FAKE, nbytes=1 << 40, out=FAKE, idx=FAKE):
+        return L.asyncspade_sparse_decode(ctypes.byref(p), FAKE, FAKE, FAKE, FAKE, idx, out, ws,
+                                          nbytes, None)
+
+    p = _dec()
+    need = L.asyncspade_sparse_decode_workspace(ctypes.byref(p))
+    # one 256-entry chunk: [B][Hq][1][D + 2] fp32 partials
+    assert need >= 2 * 32 * 1 * 130 * 4
+    assert call(p, out=None) == 1
+    assert call(p, idx=None) == 1
+    assert call(p, nbytes=need - 1) == 4
+    assert call(_dec(n_fresh=-1)) == 2
+    assert call(_dec(n_q_heads=12)) == 2
+    assert call(_dec(head_dim=80, k_stride_t=80, v_stride_t=80)) == 3
+    assert call(_dec(v_stride_h=1004)) == 1
+    assert call(_dec(sm_scale=float("nan"))) == 1

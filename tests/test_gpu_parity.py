@@ -1,0 +1,326 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, on the
+same seeded inputs, element by element.  Tolerances: tests/parity_util.py
+(BASELINE.json north star).  Chained parity feeds the oracle the GPU's own
+upstream output (GPU q_hat into the oracle's scorer, GPU idx into the
+oracle's decode) so a legitimately different near-tie upstream cannot flip
+a downstream check."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2510_07486_b200 as asp
+from paper_2510_07486_b200 import build as asp_build
+from paper_2510_07486_b200 import configs, synth
+from paper_2510_07486_b200.step import DecodeStep
+from parity_util import (ATTN_RTOL, Q_HAT_RTOL, check_selection, rel_inf_err, rows_sample)
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    asp_build.build()
+    asp.lib()
+
+
+def to_dev_bf16(bits: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(bits.view(np.int16).copy()).to(DEV).view(torch.bfloat16)
+
+
+def from_dev_bf16(t: torch.Tensor) -> np.ndarray:
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+# ----------------------------------------------------------------------------- inputs
+def test_device_generator_matches_host():
+    """The device generator (csrc/synth.cu) reproduces synth.py bit for bit,
+    including a head shard (b0/h0 offsets)."""
+    seed = synth.base_seed(1)
+    k = torch.empty(2, 3, 40, 128, dtype=torch.bfloat16, device=DEV)
+    synth.fill_kv_device(k, seed, synth.STREAM_K, 0, 5, 8)
+    host = synth.kv_cache(seed, synth.STREAM_K, 2, 3, 40, 128, h0=5, n_kv_heads_global=8)
+    np.testing.assert_array_equal(from_dev_bf16(k), host)
+    win = torch.empty(2, 4, 16, 64, dtype=torch.float32, device=DEV)
+    q = torch.empty(2, 4, 64, dtype=torch.bfloat16, device=DEV)
+    synth.fill_query_device(win, q.view(torch.int16), seed, 0, 4, 8)
+    hw, hq = synth.query_trace(seed, 2, 8, 16, 64, h0=4, head_slice=4)
+    np.testing.assert_array_equal(win.cpu().numpy(), hw)
+    np.testing.assert_array_equal(from_dev_bf16(q), hq)
+
+
+# ----------------------------------------------------------------------------- a1 predict
+PRED_FLAGS = [0, asp.ASSEMBLY_SINGLE, asp.ASSEMBLY_PER_WINDOW, asp.DOUBLE_SOFTMAX,
+              asp.SIGN_NEGATED, asp.EPS_ABSOLUTE, asp.ASSEMBLY_SINGLE | asp.NORM_NONE]
+
+
+@pytest.mark.parametrize("flags", PRED_FLAGS)
+@pytest.mark.parametrize("shape", [(1, 2, 4, 64), (32, 32, 16, 128), (3, 5, 32, 64), (2, 3, 2, 128)])
+def test_predict_parity(flags, shape):
+    B, Hq, W, D = shape
+    win, _ = synth.query_trace(synth.base_seed(1) + W, B, Hq, W, D)
+    eps = 1e-2 if not flags & asp.EPS_ABSOLUTE else 0.5
+    for ring in (0, W // 2):
+        phys = np.roll(win, ring, axis=2)        # logical j at physical (ring + j) % W
+        g = asp.predict_query(torch.from_numpy(phys).to(DEV), eps=eps, flags=flags,
+                              ring_start=ring)
+        ref, cond = oracle.predict(phys, eps, flags, ring)
+        assert cond == 0
+        err = rel_inf_err(g.cpu().numpy(), ref)
+        assert err <= Q_HAT_RTOL, err
+
+
+def test_predict_special_cases_on_gpu():
+    """Constant window -> exact; W = 1 passthrough; NaN -> flag 1 +
+    passthrough; not-PD (negative absolute eps on a zero history) -> flag 2."""
+    q = np.random.default_rng(0).standard_normal(128).astype(np.float32)
+    const = np.broadcast_to(q, (4, 3, 16, 128)).copy()
+    g = asp.predict_query(torch.from_numpy(const).to(DEV)).cpu().numpy()
+    assert np.array_equal(g, np.broadcast_to(q, (4, 3, 128)))
+    w1 = np.random.default_rng(1).standard_normal((2, 2, 1, 64)).astype(np.float32)
+    assert np.array_equal(asp.predict_query(torch.from_numpy(w1).to(DEV)).cpu().numpy(), w1[:, :, 0])
+    bad = np.ones((1, 2, 4, 64), np.float32)
+    bad[0, 1, 2, 5] = np.nan
+    flags = torch.zeros(1, dtype=torch.int32, device=DEV)
+    g = asp.predict_query(torch.from_numpy(bad).to(DEV), dev_flags=flags).cpu().numpy()
+    assert flags.item() & asp.FLAG_NONFINITE
+    assert np.array_equal(g[0, 1], bad[0, 1, 3]) and np.array_equal(g[0, 0], bad[0, 0, 3])
+    z = np.zeros((1, 1, 4, 64), np.float32)
+    z[0, 0, 3] = np.arange(64)
+    flags.zero_()
+    g = asp.predict_query(torch.from_numpy(z).to(DEV), eps=-1.0, flags=asp.EPS_ABSOLUTE,
+                          dev_flags=flags).cpu().numpy()
+    assert flags.item() & asp.FLAG_NOT_PD and np.array_equal(g[0, 0], z[0, 0, 3])
+
+
+# ----------------------------------------------------------------------------- a2+a3 select
+def _score_select_case(B, Hq, Hkv, D, L, k, seq_lens, seed, kv=None, agg=asp.AGG_MAX):
+    rng = np.random.default_rng(seed)
+    K = kv if kv is not None else synth.kv_cache(seed, synth.STREAM_K, B, Hkv, L, D)
+    qh = (rng.standard_normal((B, Hq, D)) * 0.7).astype(np.float32)
+    Kd = to_dev_bf16(K)
+    sl = torch.tensor(seq_lens, dtype=torch.int32, device=DEV)
+    scores = torch.full((B, Hkv, L), np.nan, dtype=torch.float32, device=DEV)
+    flags = torch.zeros(1, dtype=torch.int32, device=DEV)
+    idx = asp.score_select(torch.from_numpy(qh).to(DEV), Kd, sl, k, scores=scores,
+                           aggregation=agg, dev_flags=flags)
+    idx2 = asp.score_select(torch.from_numpy(qh).to(DEV), Kd, sl, k, aggregation=agg)
+    assert torch.equal(idx, idx2), "scores-buffer and workspace paths must agree"
+    s_or, _ = oracle.score(qh, K, seq_lens, agg)
+    return idx.cpu().numpy(), scores.cpu().numpy(), s_or, int(flags.item())
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+@pytest.mark.parametrize("D", [64, 128])
+def test_score_select_parity_small(G, D):
+    B, Hkv, L, k = 3, 2, 1000, 37
+    seq_lens = [1000, 777, 256]
+    idx, sg, so, flags = _score_select_case(B, Hkv * G, Hkv, D, L, k, seq_lens, 100 + G + D)
+    assert flags == 0
+    for b in range(B):
+        for h in range(Hkv):
+            n = seq_lens[b]
+            smax = np.abs(so[b, h, :n]).max()
+            assert np.abs(sg[b, h, :n] - so[b, h, :n]).max() <= 1e-5 * smax
+            check_selection(idx[b, h], so[b, h], n, k)
+
+
+def test_score_select_sum_aggregation():
+    idx, sg, so, _ = _score_select_case(2, 8, 2, 128, 513, 40, [513, 300], 7, agg=asp.AGG_SUM)
+    for b, n in enumerate([513, 300]):
+        for h in range(2):
+            check_selection(idx[b, h], so[b, h], n, 40)
+
+
+def test_score_select_short_rows_and_extremes():
+    """R13 short rows (len < k, len == k, len == 0), k = 1, ragged tail."""
+    B, Hkv, G, D, L = 5, 1, 2, 64, 300
+    seq_lens = [300, 20, 16, 0, 299]
+    idx, _, so, flags = _score_select_case(B, Hkv * G, Hkv, D, L, 16, seq_lens, 11)
+    assert flags & asp.FLAG_SHORT_ROW
+    for b in range(B):
+        check_selection(idx[b, 0], so[b, 0], seq_lens[b], 16)
+    idx1, _, so1, _ = _score_select_case(2, 2, 1, 64, 300, 1, [300, 5], 12)
+    for b, n in enumerate([300, 5]):
+        assert idx1[b, 0, 0] == int(np.argmax(so1[b, 0, :n]))
+
+
+def test_score_select_exact_ties_lower_index_wins():
+    """R9: keys drawn from a 16-row codebook -> massive exact ties; equal keys
+    must give equal GPU scores and the lowest indices must win, exactly as in
+    the oracle's brute-force sort."""
+    rng = np.random.default_rng(21)
+    B, Hkv, G, D, L, k = 2, 2, 4, 128, 4096, 700
+    book = synth.f32_to_bf16_bits(rng.standard_normal((16, D)).astype(np.float32))
+    K = book[rng.integers(0, 16, (B, Hkv, L))]
+    idx, sg, so, _ = _score_select_case(B, Hkv * G, Hkv, D, L, k, [L, L - 3], 22, kv=K)
+    ref, _ = oracle.select(so, k, np.array([[L, L], [L - 3, L - 3]]))
+    np.testing.assert_array_equal(idx, ref)
+
+
+def test_score_select_all_equal_keys():
+    K = np.zeros((1, 1, 2048, 64), np.uint16)
+    idx, _, _, _ = _score_select_case(1, 8, 1, 64, 2048, 100, [2048], 3, kv=K)
+    np.testing.assert_array_equal(idx[0, 0], np.arange(100))
+
+
+def test_score_select_long_row_global_path():
+    """Rows longer than the shared-memory key cache (40,960 tokens) take the
+    L2-streaming path."""
+    B, Hkv, G, D, L, k = 1, 1, 8, 128, 65536, 4096
+    idx, _, so, _ = _score_select_case(B, Hkv * G, Hkv, D, L, k, [L - 11], 31)
+    check_selection(idx[0, 0], so[0, 0], L - 11, k)
+
+
+# ----------------------------------------------------------------------------- a4 decode
+def _decode_case(B, Hq, Hkv, D, L, idx, seq_lens, n_fresh, seed):
+    K = synth.kv_cache(seed, synth.STREAM_K, B, Hkv, L, D)
+    V = synth.kv_cache(seed, synth.STREAM_V, B, Hkv, L, D)
+    _, q = synth.query_trace(seed, B, Hq, 2, D)
+    out = asp.sparse_decode(to_dev_bf16(q), to_dev_bf16(K), to_dev_bf16(V),
+                            torch.tensor(seq_lens, dtype=torch.int32, device=DEV),
+                            torch.from_numpy(idx).to(DEV), n_fresh=n_fresh)
+    ref = oracle.sparse_decode(q, K, V, idx, seq_lens, n_fresh)
+    return out.cpu().numpy(), ref, (q, K, V)
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("n_fresh", [0, 1, 3])
+def test_decode_parity(G, D, n_fresh):
+    rng = np.random.default_rng(G * 10 + D + n_fresh)
+    B, Hkv, L, k = 2, 2, 1500, 600                      # 600 + n_fresh entries: 3 chunks, ragged
+    seq_lens = [1500, 900]
+    idx = np.full((B, Hkv, k), -1, np.int32)
+    for b in range(B):
+        for h in range(Hkv):
+            m = min(k - 7, seq_lens[b])
+            idx[b, h, :m] = np.sort(rng.choice(seq_lens[b], m, replace=False))
+    out, ref, _ = _decode_case(B, Hkv * G, Hkv, D, L, idx, seq_lens, n_fresh, 40 + G)
+    assert rel_inf_err(out, ref) <= ATTN_RTOL
+
+
+def test_decode_full_selection_equals_dense():
+    """North star: with k = context length, sparse attention == dense."""
+    B, Hq, Hkv, D, L = 2, 8, 2, 128, 700
+    idx = np.broadcast_to(np.arange(L, dtype=np.int32), (B, Hkv, L)).copy()
+    out, ref, (q, K, V) = _decode_case(B, Hq, Hkv, D, L, idx, [L, L], 0, 5)
+    dense = oracle.dense_attention(q, K, V, [L, L])
+    assert rel_inf_err(out, dense) <= ATTN_RTOL
+    assert rel_inf_err(out, ref) <= ATTN_RTOL
+
+
+def test_decode_edge_cases():
+    """Empty set -> 0; one token -> its V row; duplicate fresh tail ignored."""
+    B, Hq, Hkv, D, L = 1, 4, 1, 64, 64
+    idx = np.full((B, Hkv, 8), -1, np.int32)
+    out, _, _ = _decode_case(B, Hq, Hkv, D, L, idx, [L], 0, 9)
+    assert np.all(out == 0)
+    idx[0, 0, 3] = 17
+    out, ref, (_, _, V) = _decode_case(B, Hq, Hkv, D, L, idx, [L], 0, 9)
+    np.testing.assert_array_equal(out[0, 0], synth.bf16_bits_to_f32(V[0, 0, 17]))
+    idx[0, 0, 4] = 63                                   # also the fresh token
+    out, ref, _ = _decode_case(B, Hq, Hkv, D, L, idx, [L], 1, 9)
+    assert rel_inf_err(out, ref) <= ATTN_RTOL
+
+
+# ----------------------------------------------------------------------------- composed step
+def _oracle_row_checks(step: DecodeStep, rows, n_fresh=0):
+    """For sampled (b, h): predict / select (band) / decode parity, chained."""
+    cfg = step.cfg
+    G, D, L, k, W = cfg.group, cfg.head_dim, cfg.seq_len, cfg.top_k, cfg.window
+    seed = synth.base_seed(cfg.index)
+    qh_g = step.q_hat.cpu().numpy()
+    idx_g = step.sel_idx.cpu().numpy()
+    out_g = step.out.cpu().numpy()
+    bands = 0
+    for r in rows:
+        b, hl = divmod(int(r), step.n_kv)
+        hg = step.h0 + hl
+        win, q = synth.query_trace(seed, cfg.batch, cfg.n_q_heads, W, D, b0=b, h0=hg * G,
+                                   batch_slice=1, head_slice=G)
+        qh_or, _ = oracle.predict(win, step.eps, step.flags)
+        assert rel_inf_err(qh_g[b, hl * G:(hl + 1) * G], qh_or[0]) <= Q_HAT_RTOL
+        K = synth.kv_rows(seed, synth.STREAM_K, b, hg, 0, L, cfg.n_kv_heads, L, D)[None, None]
+        V = synth.kv_rows(seed, synth.STREAM_V, b, hg, 0, L, cfg.n_kv_heads, L, D)[None, None]
+        s_or, _ = oracle.score(qh_g[b:b + 1, hl * G:(hl + 1) * G], K, [L])   # chained
+        bands += check_selection(idx_g[b, hl], s_or[0, 0], L - n_fresh, k)["band"]
+        o_or = oracle.sparse_decode(q, K, V, idx_g[b:b + 1, hl:hl + 1], [L], n_fresh)
+        assert rel_inf_err(out_g[b, hl * G:(hl + 1) * G], o_or[0]) <= ATTN_RTOL
+    return bands
+
+
+def test_step_tiny_all_rows():
+    step = DecodeStep(configs.TINY, DEV)
+    step.fill_synthetic()
+    step.run()
+    torch.cuda.synchronize()
+    _oracle_row_checks(step, range(configs.TINY.batch * configs.TINY.n_kv_heads))
+
+
+def test_step_qwen3_8b_sampled_rows():
+    step = DecodeStep(configs.QWEN3_8B, DEV)
+    step.fill_synthetic()
+    step.run()
+    torch.cuda.synchronize()
+    assert int(step.dev_flags.item()) == 0
+    _oracle_row_checks(step, rows_sample(step.cfg.batch * step.n_kv, 12, seed=1))
+    del step
+    torch.cuda.empty_cache()
+
+
+def test_step_qwen3_32b_graph_sampled_rows_and_determinism():
+    """Config [2] at full size in the launch configuration bench.py times
+    (CUDA-graph replay); sampled rows vs the oracle; replays bit-identical."""
+    step = DecodeStep(configs.QWEN3_32B, DEV)
+    step.fill_synthetic()
+    step.capture()
+    step.replay()
+    torch.cuda.synchronize()
+    idx1, out1 = step.sel_idx.clone(), step.out.clone()
+    step.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(idx1, step.sel_idx) and torch.equal(out1, step.out)
+    _oracle_row_checks(step, rows_sample(step.cfg.batch * step.n_kv, 8, seed=2))
+    del step
+    torch.cuda.empty_cache()
+
+
+def test_kv_head_shards_bit_identical():
+    """§8(e): P = 2 KV-head shards reproduce the P = 1 slices bit for bit."""
+    cfg = configs.QWEN3_8B.with_(batch=4, seq_len=8192, top_k=512)
+    full = DecodeStep(cfg, DEV)
+    full.fill_synthetic()
+    full.run()
+    G = cfg.group
+    for r in range(2):
+        part = DecodeStep(cfg, DEV, kv_heads=(r * 4, 4))
+        part.fill_synthetic()
+        part.run()
+        torch.cuda.synchronize()
+        assert torch.equal(part.sel_idx, full.sel_idx[:, r * 4:(r + 1) * 4])
+        assert torch.equal(part.out, full.out[:, r * 4 * G:(r + 1) * 4 * G])
+        assert torch.equal(part.q_hat, full.q_hat[:, r * 4 * G:(r + 1) * 4 * G])
+
+
+def test_step_with_fresh_token():
+    cfg = configs.QWEN3_8B.with_(batch=2, seq_len=4096, top_k=256)
+    step = DecodeStep(cfg, DEV, n_fresh=1)
+    step.fill_synthetic()
+    step.run()
+    torch.cuda.synchronize()
+    # selection saw all L tokens; decode skips idx in the fresh tail and adds it once
+    cfg_rows = rows_sample(cfg.batch * cfg.n_kv_heads, 4, seed=3)
+    seed = synth.base_seed(cfg.index)
+    out_g = step.out.cpu().numpy()
+    idx_g = step.sel_idx.cpu().numpy()
+    for r in cfg_rows:
+        b, h = divmod(int(r), cfg.n_kv_heads)
+        G, D, L = cfg.group, cfg.head_dim, cfg.seq_len
+        _, q = synth.query_trace(seed, cfg.batch, cfg.n_q_heads, cfg.window, D, b0=b,
+                                 h0=h * G, batch_slice=1, head_slice=G)
+        K = synth.kv_rows(seed, synth.STREAM_K, b, h, 0, L, cfg.n_kv_heads, L, D)[None, None]
+        V = synth.kv_rows(seed, synth.STREAM_V, b, h, 0, L, cfg.n_kv_heads, L, D)[None, None]
+        o_or = oracle.sparse_decode(q, K, V, idx_g[b:b + 1, h:h + 1], [L], 1)
+        assert rel_inf_err(out_g[b, h * G:(h + 1) * G], o_or[0]) <= ATTN_RTOL

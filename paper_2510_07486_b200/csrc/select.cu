@@ -24,13 +24,15 @@ constexpr int kBins = 4096;
 struct SelectSmem {
     uint32_t hist[kBins];
     uint32_t warp_tot[kWarps];
+    uint32_t scan_total;
     uint32_t found_bin, found_rem;
     uint32_t keys[kSmemKeys];
 };
 
 // Block-wide exclusive scan of one uint32 per thread; returns the exclusive
-// prefix and writes the block total to *total.
-__device__ uint32_t block_excl_scan(uint32_t v, uint32_t *warp_tot, uint32_t *total) {
+// prefix and writes the block total to *total (every thread).
+__device__ uint32_t block_excl_scan(uint32_t v, uint32_t *warp_tot, uint32_t *total_smem,
+                                    uint32_t *total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t x = v;
 #pragma unroll
@@ -49,11 +51,12 @@ __device__ uint32_t block_excl_scan(uint32_t v, uint32_t *warp_tot, uint32_t *to
             if (lane >= o) s += y;
         }
         warp_tot[lane] = s - t;              // exclusive warp offsets
-        if (lane == 31) *total = s;
+        if (lane == 31) *total_smem = s;
     }
     __syncthreads();
     const uint32_t r = warp_tot[warp] + x - v;
-    __syncthreads();                         // warp_tot reusable after return
+    *total = *total_smem;
+    __syncthreads();                         // warp_tot / total reusable after return
     return r;
 }
 
@@ -68,7 +71,7 @@ __device__ void find_bucket(SelectSmem &s, int nbins, uint32_t k_rem, uint32_t *
     const bool owns = t * per < nbins;
     if (owns)
         for (int i = 0; i < per; i++) local += s.hist[nbins - 1 - (t * per + i)];
-    uint32_t above = block_excl_scan(local, s.warp_tot, total);
+    uint32_t above = block_excl_scan(local, s.warp_tot, &s.scan_total, total);
     if (owns) {
         for (int i = 0; i < per; i++) {
             const int bin = nbins - 1 - (t * per + i);
@@ -167,7 +170,7 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
             eq = key == T;
         }
         const uint32_t packed = (eq << 16) | gt;
-        const uint32_t excl = block_excl_scan(packed, s.warp_tot, &total);
+        const uint32_t excl = block_excl_scan(packed, s.warp_tot, &s.scan_total, &total);
         const uint32_t eq_before = carry_eq + (excl >> 16);
         const uint32_t gt_before = carry_gt + (excl & 0xFFFFu);
         if (gt || (eq && eq_before < need)) out[gt_before + min(eq_before, need)] = i;

@@ -72,14 +72,14 @@ __global__ void query_kernel(uint64_t key, float *window, uint16_t *q, int bs, i
 
 extern "C" {
 
-int asp_synth_kv(uint64_t stream_key, uint16_t *dst, int bs, int hs, int L, int D, int b0, int h0,
+__attribute__((visibility("default"))) int asp_synth_kv(uint64_t stream_key, uint16_t *dst, int bs, int hs, int L, int D, int b0, int h0,
                  int hg, long long sb, long long sh, long long st, void *stream) {
     kv_kernel<<<4096, 256, 0, (cudaStream_t)stream>>>(stream_key, dst, bs, hs, L, D, b0, h0, hg,
                                                       sb, sh, st);
     return (int)cudaGetLastError();
 }
 
-int asp_synth_query(uint64_t stream_key, float *window, uint16_t *q, int bs, int hs, int W, int D,
+__attribute__((visibility("default"))) int asp_synth_query(uint64_t stream_key, float *window, uint16_t *q, int bs, int hs, int W, int D,
                     int b0, int h0, int hg, void *stream) {
     query_kernel<<<1024, 256, 0, (cudaStream_t)stream>>>(stream_key, window, q, bs, hs, W, D, b0,
                                                          h0, hg);

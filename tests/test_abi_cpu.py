@@ -122,3 +122,10 @@ def test_sparse_decode_validation_and_workspace(L):
     assert call(_dec(head_dim=80, k_stride_t=80, v_stride_t=80)) == 3
     assert call(_dec(v_stride_h=1004)) == 1
     assert call(_dec(sm_scale=float("nan"))) == 1
+
+
+def test_synth_library_exports():
+    """The bench/test input generator library loads and exports its two calls."""
+    from paper_2510_07486_b200 import synth
+    L = synth._dev_lib()
+    assert hasattr(L, "asp_synth_kv") and hasattr(L, "asp_synth_query")

@@ -1,6 +1,7 @@
 // common.cuh -- small device helpers shared by the sm_100a kernels of the
 // product path.  (Nothing here is shared with oracle/.)
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 

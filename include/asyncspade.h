@@ -180,13 +180,16 @@ ASP_API asp_status asyncspade_score_select(const asp_select_params *p, const flo
  * in a fixed order.  An empty set gives out = 0.
  *
  * q         device bf16 [batch][n_q_heads][head_dim].
- * k_cache, v_cache  device bf16, strided like asp_select_params' K.
+ * k_cache, v_cache  device bf16, strided like asp_select_params' K; rows
+ *           are gathered by TMA, so stride_b and stride_h must be multiples
+ *           of stride_t (ASP_ERR_UNSUPPORTED otherwise).  max_seq_len bounds
+ *           every seq_lens[b] (the cache capacity).
  * seq_lens  device int32 [batch].   sel_idx device int32 [batch][n_kv_heads][top_k].
  * out       device fp32 [batch][n_q_heads][head_dim], written.
  * workspace device, >= asyncspade_sparse_decode_workspace(p) bytes.
  * ---------------------------------------------------------------------- */
 typedef struct {
-    int32_t batch, n_q_heads, n_kv_heads, head_dim, top_k, n_fresh;
+    int32_t batch, n_q_heads, n_kv_heads, head_dim, top_k, n_fresh, max_seq_len;
     float sm_scale; /* usually 1/sqrt(head_dim) */
     int64_t k_stride_b, k_stride_h, k_stride_t, v_stride_b, v_stride_h, v_stride_t;
 } asp_decode_params;

@@ -54,7 +54,7 @@ class DecodeParams(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int32), ("n_q_heads", ctypes.c_int32),
                 ("n_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
                 ("top_k", ctypes.c_int32), ("n_fresh", ctypes.c_int32),
-                ("sm_scale", ctypes.c_float),
+                ("max_seq_len", ctypes.c_int32), ("sm_scale", ctypes.c_float),
                 ("k_stride_b", ctypes.c_int64), ("k_stride_h", ctypes.c_int64),
                 ("k_stride_t", ctypes.c_int64), ("v_stride_b", ctypes.c_int64),
                 ("v_stride_h", ctypes.c_int64), ("v_stride_t", ctypes.c_int64)]
@@ -142,12 +142,12 @@ def select_params(q_hat: torch.Tensor, k_cache: torch.Tensor, top_k: int,
 def decode_params(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, top_k: int,
                   n_fresh: int = 0, sm_scale: float | None = None) -> DecodeParams:
     B, Hq, D = q.shape
-    _, Hkv, _, _ = k_cache.shape
+    _, Hkv, L, _ = k_cache.shape
     if k_cache.stride(3) != 1 or v_cache.stride(3) != 1:
         raise AsyncSpadeError("caches must have unit stride along head_dim")
     if sm_scale is None:
         sm_scale = D ** -0.5
-    return DecodeParams(B, Hq, Hkv, D, top_k, n_fresh, sm_scale, *k_cache.stride()[:3],
+    return DecodeParams(B, Hq, Hkv, D, top_k, n_fresh, L, sm_scale, *k_cache.stride()[:3],
                         *v_cache.stride()[:3])
 
 

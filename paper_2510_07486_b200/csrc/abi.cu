@@ -30,7 +30,7 @@ asp_status check_select(const asp_select_params *p) {
 asp_status check_decode(const asp_decode_params *p) {
     if (!p) return ASP_ERR_INVALID_ARGUMENT;
     if (p->batch <= 0 || p->n_q_heads <= 0 || p->n_kv_heads <= 0 || p->head_dim <= 0 ||
-        p->top_k <= 0 || p->n_fresh < 0)
+        p->top_k <= 0 || p->n_fresh < 0 || p->max_seq_len <= 0)
         return ASP_ERR_SHAPE;
     if (p->n_q_heads % p->n_kv_heads) return ASP_ERR_SHAPE;
     if (!dim_ok(p->head_dim) || !group_ok(p->n_q_heads / p->n_kv_heads)) return ASP_ERR_UNSUPPORTED;
@@ -41,6 +41,10 @@ asp_status check_decode(const asp_decode_params *p) {
     if ((p->k_stride_b | p->k_stride_h | p->k_stride_t | p->v_stride_b | p->v_stride_h |
          p->v_stride_t) & 7)
         return ASP_ERR_INVALID_ARGUMENT;
+    // the gather views each cache as [rows][head_dim] with row stride stride_t
+    if (p->k_stride_b % p->k_stride_t || p->k_stride_h % p->k_stride_t ||
+        p->v_stride_b % p->v_stride_t || p->v_stride_h % p->v_stride_t)
+        return ASP_ERR_UNSUPPORTED;
     return ASP_OK;
 }
 

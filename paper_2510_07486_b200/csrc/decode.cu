@@ -5,169 +5,418 @@
 //   out[b,hq] = sum_j softmax_j(sm_scale * q[b,hq] . K[b,h,t_j]) V[b,h,t_j],
 //   t_j in {sel_idx valid} U [len - n_fresh, len),  h = hq / G.
 //
-// Design (B200), split-K: the E = top_k + n_fresh entries of a (b, KV head)
-// row are cut into fixed 256-entry chunks, one CTA (4 warps x 64 entries) per
-// chunk, so a row's arithmetic order depends only on (top_k, n_fresh).  All G
-// query heads of the KV head share each gathered K/V row (GQA reuse).  Within
-// a warp, lane j owns entry j of a 32-entry block: it gathers its key row with
-// 16-B loads, computes the G logits in fp32 (bf16 x bf16 products are exact),
-// and the block updates a running (max, sum) per head with warp-shuffle
-// reductions; the value rows are then streamed coalesced (lane = 4 dims) and
-// accumulated with per-entry weights broadcast by shuffle.  Warps, then
-// chunks, are merged by the log-sum-exp rule in a fixed order; the chunk merge
-// is a second small kernel.
+// Design (B200): split-K over fixed 256-entry chunks of a (b, KV head) row --
+// a chunk's arithmetic depends only on the row, never on the grid -- with
+// the chunk partials merged in chunk order by a small combine kernel.  Each
+// chunk is one work item of a persistent, warp-specialised kernel:
+//
+//   warp 0   TMA producer: resolves the chunk's token list and GATHERS the
+//            selected key / value rows straight into 128-B-swizzled shared
+//            memory with cp.async.bulk.tensor tile::gather4 (4 rows per
+//            instruction, one per lane), 128-token tiles, 5-stage ring;
+//   warp 1   TMEM owner + single-thread tcgen05.mma issuer:
+//              S^T[128 tok x 16] = K_tile . Q^T          (q is bf16: exact)
+//              O^T[D x 16]      += V_tile^T . P^T        (V tile MN-major)
+//            P = [p_hi; p_lo] is the fp32 softmax weight split into two bf16
+//            terms (rel. error 2^-17), so the P.V products stay fp32-exact;
+//   warp 2   builds the bf16 Q operand when the row changes;
+//   warps 4-7  softmax (chunk max / exp2 / sums with warp shuffles and one
+//            named barrier) writing the P operand, then the epilogue that
+//            drains O from TMEM and stores the chunk partial (m, l, o).
+//
+// All G query heads of a KV head share every gathered row (GQA reuse); the
+// contraction runs on the tensor cores so the SM pipes only orchestrate the
+// gather stream (537 MB of K/V rows at the Qwen3-32B shape).
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace {
 
-constexpr int kThreads = 128;
-constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 256;                   // entries per CTA (fixed: determinism)
-constexpr int kPerWarp = kChunk / kWarps;     // 64
+using namespace asp::tc;
+
+constexpr int kTile = 128;                  // tokens per tile
+constexpr int kChunk = 256;                 // entries per work item (fixed: determinism)
+constexpr int kTilesPerItem = kChunk / kTile;
+constexpr int kN = 16;                      // MMA N: G heads (MMA1) / 2G hi-lo rows (MMA2)
+constexpr int kProducerWarps = 4;
+constexpr int kProducerThreads = kProducerWarps * 32;
+constexpr int kMmaWarp = 8;
+constexpr int kThreads = 9 * 32;             // 4 producer, 4 softmax/epilogue, 1 MMA warp
 constexpr float kLog2e = 1.4426950408889634f;
 
+template <int D>
+struct DCfg {
+    static constexpr int kRegions = D / 64;
+    static constexpr int kStageBytes = kRegions * kTile * 128;      // one K or V tile
+    static constexpr int kStages = D == 128 ? 5 : 8;
+    static constexpr int kQSlotBytes = kRegions * kN * 128;
+    static constexpr int kPTileBytes = 2 * kN * 128;                // 128 tokens = 2 regions
+    static constexpr int kPSlotBytes = kTilesPerItem * kPTileBytes;
+    static constexpr int kZeroBytes = D == 64 ? 16384 : 0;          // MN-block 1 of V^T for D=64
+    static constexpr int kTokBytes = 2 * kChunk * 4;
+    static constexpr int kRedBytes = 2 * 2 * 4 * 8 * 4 + 2 * 8 * 4; // wmax, wsum, mrow
+    static constexpr int kBarBytes = 256;
+    static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 2 * kQSlotBytes +
+                                      2 * kPSlotBytes + kZeroBytes + kTokBytes + kRedBytes +
+                                      kBarBytes;
+};
+
+struct Item {
+    int row, chunk;
+};
+
 template <int D, int G>
-__global__ void __launch_bounds__(kThreads)
-decode_partial_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
-                      const asp_bf16 *__restrict__ k_cache, const asp_bf16 *__restrict__ v_cache,
-                      const int32_t *__restrict__ seq_lens, const int32_t *__restrict__ sel_idx,
-                      float *__restrict__ partials, int n_splits) {
-    constexpr int DL = D / 32;               // dims per lane in the PV phase (4 or 2)
-    __shared__ __align__(16) float qs[G][D];
-    __shared__ float wm[kWarps][G], wl[kWarps][G];
-    __shared__ __align__(16) float wo[kWarps][G][D];
+__global__ void __launch_bounds__(kThreads, 1)
+decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
+                 const asp_bf16 *__restrict__ k_cache, const asp_bf16 *__restrict__ v_cache,
+                 const int32_t *__restrict__ seq_lens, const int32_t *__restrict__ sel_idx,
+                 float *__restrict__ partials, int n_splits) {
+    using C = DCfg<D>;
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    unsigned char *gb = smem_raw + (base - raw);
+    // ---- shared memory carve-up (all operand regions 1024-B aligned)
+    const uint32_t stage0 = base;
+    const uint32_t qslot0 = stage0 + C::kStages * C::kStageBytes;
+    const uint32_t pslot0 = qslot0 + 2 * C::kQSlotBytes;
+    const uint32_t zero0 = pslot0 + 2 * C::kPSlotBytes;
+    const uint32_t tok0 = zero0 + C::kZeroBytes;
+    const uint32_t red0 = tok0 + C::kTokBytes;
+    const uint32_t bar0 = red0 + C::kRedBytes;
+    int32_t *s_tok = reinterpret_cast<int32_t *>(gb + (tok0 - base));          // [2][256]
+    float *s_wmax = reinterpret_cast<float *>(gb + (red0 - base));             // [2][4][8]
+    float *s_wsum = s_wmax + 2 * 4 * 8;                                        // [2][4][8]
+    float *s_mrow = s_wsum + 2 * 4 * 8;                                        // [2][8]
+    auto bar = [&](int i) { return bar0 + 8u * i; };
+    // barrier indices
+    const int B_FULL = 0, B_EMPTY = C::kStages;
+    const int B_QFULL = 2 * C::kStages, B_QEMPTY = B_QFULL + 2;
+    const int B_TOKFULL = B_QEMPTY + 2, B_TOKEMPTY = B_TOKFULL + 2;
+    const int B_SFULL = B_TOKEMPTY + 2, B_PFULL = B_SFULL + 2;
+    const int B_OFULL = B_PFULL + 2, B_OEMPTY = B_OFULL + 2;
+    const int B_COUNT = B_OEMPTY + 2;
+    const uint32_t tmem_holder = bar(B_COUNT);
+    volatile uint32_t *tmem_holder_g = reinterpret_cast<volatile uint32_t *>(gb + (tmem_holder - base));
 
-    const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int Hq = p.n_q_heads;
-    const float scale = p.sm_scale * kLog2e;
-    const asp_bf16 *qsrc = q + ((size_t)b * Hq + (size_t)h * G) * D;
-    for (int i = threadIdx.x; i < G * D; i += kThreads) qs[i / D][i % D] = asp::bf16f(qsrc[i]);
-    __syncthreads();
-
-    const int len = seq_lens[b];
-    const int fresh_lo = max(len - p.n_fresh, 0);
+    const int Hq = p.n_q_heads, Hkv = p.n_kv_heads;
     const int E = p.top_k + p.n_fresh;
-    const asp_bf16 *kb = k_cache + (size_t)b * p.k_stride_b + (size_t)h * p.k_stride_h;
-    const asp_bf16 *vb = v_cache + (size_t)b * p.v_stride_b + (size_t)h * p.v_stride_h;
-    const int32_t *ib = sel_idx + ((size_t)b * p.n_kv_heads + h) * p.top_k;
+    const long total = (long)p.batch * Hkv * n_splits;
+    const long i_start = total * blockIdx.x / gridDim.x;
+    const long i_end = total * (blockIdx.x + 1) / gridDim.x;
+    const int n_items = (int)(i_end - i_start);
+    auto item = [&](int i) -> Item {
+        const long g = i_start + i;
+        return Item{(int)(g / n_splits), (int)(g % n_splits)};
+    };
 
-    float m[G], l[G], o[G][DL];
-#pragma unroll
-    for (int g = 0; g < G; g++) {
-        m[g] = -INFINITY;
-        l[g] = 0.0f;
-#pragma unroll
-        for (int i = 0; i < DL; i++) o[g][i] = 0.0f;
-    }
-
-    for (int blk = 0; blk < kPerWarp / 32; blk++) {
-        const int e = split * kChunk + warp * kPerWarp + blk * 32 + lane;
-        int tok = -1;
-        if (e < p.top_k) {
-            const int t = ib[e];
-            if (t >= 0 && t < fresh_lo) tok = t;
-        } else if (e < E) {
-            const int t = fresh_lo + (e - p.top_k);
-            if (t < len) tok = t;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::kStages; s++) {
+            mbar_init(bar(B_FULL + s), kProducerThreads);   // one cp.async arrival per producer
+            mbar_init(bar(B_EMPTY + s), 1);
         }
-        const unsigned valid_mask = __ballot_sync(0xffffffffu, tok >= 0);
-        if (valid_mask == 0u) continue;
-        // logits for this lane's entry, all G heads (log2 domain)
-        float lg[G];
-#pragma unroll
-        for (int g = 0; g < G; g++) lg[g] = 0.0f;
-        if (tok >= 0) {
-            const uint4 *kr = reinterpret_cast<const uint4 *>(kb + (size_t)tok * p.k_stride_t);
+        for (int s = 0; s < 2; s++) {
+            mbar_init(bar(B_QFULL + s), 1);
+            mbar_init(bar(B_QEMPTY + s), 1);
+            mbar_init(bar(B_TOKFULL + s), 1);
+            mbar_init(bar(B_TOKEMPTY + s), 4);
+            mbar_init(bar(B_SFULL + s), 1);
+            mbar_init(bar(B_PFULL + s), 4);
+            mbar_init(bar(B_OFULL + s), 1);
+            mbar_init(bar(B_OEMPTY + s), 4);
+        }
+        fence_mbar_init();
+    }
+    // zero the P operand slots (rows >= 2G stay zero) and the D=64 zero region
+    for (uint32_t o = threadIdx.x * 16; o < 2u * C::kPSlotBytes + C::kZeroBytes; o += kThreads * 16)
+        *reinterpret_cast<uint4 *>(gb + (pslot0 - base) + o) = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+    if (warp == kMmaWarp) tmem_alloc<128>(tmem_holder);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder_g;
+    // TMEM columns: S[slot][tile] at slot*32 + tile*16, O[slot] at 64 + slot*16
+    auto s_col = [](int slot, int t) { return (uint32_t)(slot * 32 + t * 16); };
+    auto o_col = [](int slot) { return (uint32_t)(64 + slot * 16); };
+
+    if (warp < kProducerWarps) {
+        // ================================================= producers (4 warps)
+        // Gather the selected K / V rows with cp.async (16 B per thread-op, one
+        // token row per 16 consecutive lanes -> coalesced 256-B rows) straight into
+        // the 128-B-swizzled UMMA layout; completion arrives on the stage's
+        // mbarrier (cp.async.mbarrier.arrive.noinc).  Also builds the Q operand.
+        const int pt = threadIdx.x;                           // 0..127
+        int s = 0, qs = -1, cur_row = -1;
+        uint32_t ph = 0, qph = 0;
+        auto prepare = [&](int i) {
+            const int slot = i & 1;
+            const Item it = item(i);
+            const int b = it.row / Hkv, h = it.row % Hkv;
+            const bool new_row = it.row != cur_row;
+            if (new_row) {                                    // new row: Q operand
+                qs = (qs + 1) & 1;
+                if (qs == 0 && cur_row != -1) qph ^= 1;
+                cur_row = it.row;
+                mbar_wait(bar(B_QEMPTY + qs), qph ^ 1);
+                const asp_bf16 *qsrc = q + ((size_t)b * Hq + (size_t)h * G) * D;
+                unsigned char *qslot = gb + (qslot0 - base) + qs * C::kQSlotBytes;
+                for (int c = pt; c < kN * D / 8; c += kProducerThreads) {
+                    const int n = c / (D / 8), d0 = (c % (D / 8)) * 8;
+                    uint4 v = make_uint4(0, 0, 0, 0);
+                    if (n < G) v = *reinterpret_cast<const uint4 *>(qsrc + n * D + d0);
+                    const int region = d0 / 64, chunk = (d0 % 64) / 8;
+                    *reinterpret_cast<uint4 *>(qslot + region * (kN * 128) + n * 128 +
+                                               ((chunk ^ (n & 7)) * 16)) = v;
+                }
+                fence_proxy_async_smem();
+            }
+            mbar_wait(bar(B_TOKEMPTY + slot), ((i >> 1) & 1) ^ 1);
+            const int len = min(max(seq_lens[b], 0), p.max_seq_len);
+            const int fresh_lo = max(len - p.n_fresh, 0);
+            const int32_t *ib = sel_idx + (size_t)it.row * p.top_k;
+            for (int j = pt; j < kChunk; j += kProducerThreads) {
+                const int e = it.chunk * kChunk + j;
+                int tok = -1;
+                if (e < p.top_k) {
+                    const int t = ib[e];
+                    if (t >= 0 && t < fresh_lo) tok = t;
+                } else if (e < E) {
+                    const int t = fresh_lo + (e - p.top_k);
+                    if (t < len) tok = t;
+                }
+                s_tok[slot * kChunk + j] = tok;
+            }
+            asm volatile("bar.sync 2, %0;" ::"n"(kProducerThreads) : "memory");
+            if (pt == 0) {
+                mbar_arrive(bar(B_TOKFULL + slot));
+                if (new_row) mbar_arrive(bar(B_QFULL + qs));
+            }
+        };
+        auto load = [&](int i, const asp_bf16 *cache, int64_t sb, int64_t sh, int64_t st) {
+            const int slot = i & 1;
+            const Item it = item(i);
+            const int b = it.row / Hkv, h = it.row % Hkv;
+            const asp_bf16 *rowbase = cache + b * sb + h * sh;
+            constexpr int kChunksPerRow = D / 8;              // 16-B chunks per token row
+            constexpr int kRowsPerPass = kProducerThreads / kChunksPerRow;
+            const int chunk = pt % kChunksPerRow;
+            const int region = chunk / 8, cc = chunk % 8;
+            for (int t = 0; t < kTilesPerItem; t++) {
+                mbar_wait(bar(B_EMPTY + s), ph ^ 1);
+                const uint32_t stage = stage0 + s * C::kStageBytes + region * (kTile * 128);
+                const int32_t *tk = s_tok + slot * kChunk + t * kTile;
 #pragma unroll 4
-            for (int c = 0; c < D / 8; c++) {
-                const uint4 w = __ldg(kr + c);
-                const float kk[8] = {asp::bf16lo(w.x), asp::bf16hi(w.x), asp::bf16lo(w.y),
-                                     asp::bf16hi(w.y), asp::bf16lo(w.z), asp::bf16hi(w.z),
-                                     asp::bf16lo(w.w), asp::bf16hi(w.w)};
+                for (int r = pt / kChunksPerRow; r < kTile; r += kRowsPerPass) {
+                    const int tok = max(tk[r], 0);            // invalid entries read token 0
+                    const asp_bf16 *src = rowbase + (int64_t)tok * st + chunk * 8;
+                    const uint32_t dst = stage + r * 128 + ((cc ^ (r & 7)) * 16);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src)
+                                 : "memory");
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar(B_FULL + s))
+                             : "memory");
+                if (++s == C::kStages) { s = 0; ph ^= 1; }
+            }
+        };
+        if (n_items > 0) {
+            prepare(0);
+            load(0, k_cache, p.k_stride_b, p.k_stride_h, p.k_stride_t);
+        }
+        for (int i = 0; i < n_items; i++) {
+            if (i + 1 < n_items) {
+                prepare(i + 1);
+                load(i + 1, k_cache, p.k_stride_b, p.k_stride_h, p.k_stride_t);
+            }
+            load(i, v_cache, p.v_stride_b, p.v_stride_h, p.v_stride_t);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+    } else if (warp == kMmaWarp) {
+        // ================================================= MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc1 = idesc_bf16_f32(kTile, kN);                 // K-major A, B
+            constexpr uint32_t idesc2 = idesc_bf16_f32(kTile, kN) | (1u << 15);    // A MN-major
+            int s = 0, qs = -1, cur_row = -1;
+            uint32_t ph = 0, qph = 0;
+            auto wait_stage = [&]() {
+                mbar_wait(bar(B_FULL + s), ph);
+                fence_proxy_async_smem();        // cp.async (generic proxy) -> tensor core reads
+                tc_fence_after();
+            };
+            auto mma1 = [&](int i) {
+                const int slot = i & 1;
+                const Item it = item(i);
+                if (it.row != cur_row) {
+                    if (qs >= 0) mma_commit(bar(B_QEMPTY + qs));
+                    qs = (qs + 1) & 1;
+                    if (qs == 0 && cur_row != -1) qph ^= 1;
+                    mbar_wait(bar(B_QFULL + qs), qph);
+                    cur_row = it.row;
+                }
+                const uint32_t qb = qslot0 + qs * C::kQSlotBytes;
+                for (int t = 0; t < kTilesPerItem; t++) {
+                    wait_stage();
+                    const uint32_t ab = stage0 + s * C::kStageBytes;
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; kk++) {
+                        const int r = kk / 4, ko = (kk % 4) * 32;
+                        mma_bf16(tmem_base + s_col(slot, t),
+                                 desc_sw128_kmajor(ab + r * (kTile * 128) + ko),
+                                 desc_sw128_kmajor(qb + r * (kN * 128) + ko), idesc1, kk > 0 ? 1u : 0u);
+                    }
+                    mma_commit(bar(B_EMPTY + s));
+                    if (++s == C::kStages) { s = 0; ph ^= 1; }
+                }
+                mma_commit(bar(B_SFULL + slot));
+            };
+            auto mma2 = [&](int i) {
+                const int slot = i & 1;
+                const uint32_t use = (uint32_t)((i >> 1) & 1);
+                mbar_wait(bar(B_PFULL + slot), use);
+                mbar_wait(bar(B_OEMPTY + slot), use ^ 1);
+                tc_fence_after();
+                const uint32_t pb = pslot0 + slot * C::kPSlotBytes;
+                for (int t = 0; t < kTilesPerItem; t++) {
+                    wait_stage();
+                    const uint32_t vb = stage0 + s * C::kStageBytes;
+                    // V tile as the MN-major A operand of O^T = V^T P^T: MN blocks of 64
+                    // dims (LBO) and 8-token swizzle atoms (SBO = 1024 B)
+                    const uint32_t lbo = D == 128 ? (uint32_t)(kTile * 128) : (zero0 - vb);
+#pragma unroll
+                    for (int kk = 0; kk < kTile / 16; kk++) {
+                        uint64_t ad = desc_sw128_kmajor(vb + kk * 2048);
+                        ad = (ad & ~(0x3FFFull << 16)) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16);
+                        const uint64_t bd = desc_sw128_kmajor(pb + t * C::kPTileBytes +
+                                                              (kk / 4) * (kN * 128) + (kk % 4) * 32);
+                        mma_bf16(tmem_base + o_col(slot), ad, bd, idesc2, (t | kk) ? 1u : 0u);
+                    }
+                    mma_commit(bar(B_EMPTY + s));
+                    if (++s == C::kStages) { s = 0; ph ^= 1; }
+                }
+                mma_commit(bar(B_OFULL + slot));
+            };
+            if (n_items > 0) mma1(0);
+            for (int i = 0; i < n_items; i++) {
+                if (i + 1 < n_items) mma1(i + 1);
+                mma2(i);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ================================================= softmax + epilogue (warps 4-7)
+        const int quad = warp & 3;
+        const float scale = p.sm_scale * kLog2e;
+        auto softmax = [&](int i) {
+            const int slot = i & 1;
+            const uint32_t use = (uint32_t)((i >> 1) & 1);
+            mbar_wait(bar(B_TOKFULL + slot), use);
+            mbar_wait(bar(B_SFULL + slot), use);
+            tc_fence_after();
+            float l[kTilesPerItem][G];
+            int tok[kTilesPerItem];
+#pragma unroll
+            for (int t = 0; t < kTilesPerItem; t++) {
+                uint32_t r[16];
+                tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + s_col(slot, t), r);
+                tmem_wait_ld();
+                tok[t] = s_tok[slot * kChunk + t * kTile + quad * 32 + lane];
+#pragma unroll
+                for (int g = 0; g < G; g++)
+                    l[t][g] = tok[t] >= 0 ? __uint_as_float(r[g]) * scale : -INFINITY;
+            }
+            float mx[G];
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                float m = l[0][g];
+#pragma unroll
+                for (int t = 1; t < kTilesPerItem; t++) m = fmaxf(m, l[t][g]);
+                mx[g] = asp::warp_max(m);
+            }
+            if (lane == 0)
+#pragma unroll
+                for (int g = 0; g < G; g++) s_wmax[(slot * 4 + quad) * 8 + g] = mx[g];
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            float M[G];
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                float m = s_wmax[(slot * 4 + 0) * 8 + g];
+#pragma unroll
+                for (int w = 1; w < 4; w++) m = fmaxf(m, s_wmax[(slot * 4 + w) * 8 + g]);
+                M[g] = m;
+            }
+            unsigned char *pb = gb + (pslot0 - base) + slot * C::kPSlotBytes;
+            const int x = quad * 32 + lane;                      // token column within a tile
+            const int region = x / 64, within = x % 64;
+            float sum[G];
+#pragma unroll
+            for (int g = 0; g < G; g++) sum[g] = 0.0f;
+#pragma unroll
+            for (int t = 0; t < kTilesPerItem; t++) {
+                unsigned char *ptile = pb + t * C::kPTileBytes + region * (kN * 128);
 #pragma unroll
                 for (int g = 0; g < G; g++) {
-                    const float4 qa = *reinterpret_cast<const float4 *>(&qs[g][c * 8]);
-                    const float4 qb = *reinterpret_cast<const float4 *>(&qs[g][c * 8 + 4]);
-                    float a = lg[g];
-                    a = fmaf(qa.x, kk[0], a); a = fmaf(qa.y, kk[1], a);
-                    a = fmaf(qa.z, kk[2], a); a = fmaf(qa.w, kk[3], a);
-                    a = fmaf(qb.x, kk[4], a); a = fmaf(qb.y, kk[5], a);
-                    a = fmaf(qb.z, kk[6], a); a = fmaf(qb.w, kk[7], a);
-                    lg[g] = a;
+                    const float pv = (tok[t] >= 0 && M[g] != -INFINITY) ? exp2f(l[t][g] - M[g]) : 0.0f;
+                    sum[g] += pv;
+                    const __nv_bfloat16 hi = __float2bfloat16_rn(pv);
+                    const __nv_bfloat16 lo = __float2bfloat16_rn(pv - __bfloat162float(hi));
+                    const int nh = g, nl = G + g;
+                    *reinterpret_cast<__nv_bfloat16 *>(
+                        ptile + nh * 128 + (((within >> 3) ^ (nh & 7)) * 16) + (within & 7) * 2) = hi;
+                    *reinterpret_cast<__nv_bfloat16 *>(
+                        ptile + nl * 128 + (((within >> 3) ^ (nl & 7)) * 16) + (within & 7) * 2) = lo;
                 }
             }
 #pragma unroll
-            for (int g = 0; g < G; g++) lg[g] *= scale;
-        } else {
+            for (int g = 0; g < G; g++) sum[g] = asp::warp_sum(sum[g]);
+            if (lane == 0)
 #pragma unroll
-            for (int g = 0; g < G; g++) lg[g] = -INFINITY;
-        }
-        // block-wise online softmax update
-        float pw[G];
-#pragma unroll
-        for (int g = 0; g < G; g++) {
-            const float mb = asp::warp_max(lg[g]);
-            const float mn = fmaxf(m[g], mb);
-            const float alpha = exp2f(m[g] - mn);      // m = -inf first time -> 0
-            pw[g] = (tok >= 0) ? exp2f(lg[g] - mn) : 0.0f;
-            l[g] = l[g] * alpha + asp::warp_sum(pw[g]);
-#pragma unroll
-            for (int i = 0; i < DL; i++) o[g][i] *= alpha;
-            m[g] = mn;
-        }
-        // PV: stream the value rows of the block's valid entries
-        unsigned mask = valid_mask;
-        while (mask) {
-            const int j = __ffs(mask) - 1;
-            mask &= mask - 1;
-            const int tj = __shfl_sync(0xffffffffu, tok, j);
-            const asp_bf16 *vr = vb + (size_t)tj * p.v_stride_t + lane * DL;
-            float vv[DL];
-            if constexpr (DL == 4) {
-                const uint2 w = __ldg(reinterpret_cast<const uint2 *>(vr));
-                vv[0] = asp::bf16lo(w.x); vv[1] = asp::bf16hi(w.x);
-                vv[2] = asp::bf16lo(w.y); vv[3] = asp::bf16hi(w.y);
-            } else {
-                const uint32_t w = __ldg(reinterpret_cast<const uint32_t *>(vr));
-                vv[0] = asp::bf16lo(w); vv[1] = asp::bf16hi(w);
+                for (int g = 0; g < G; g++) s_wsum[(slot * 4 + quad) * 8 + g] = sum[g];
+            if (quad == 0 && lane < G) s_mrow[slot * 8 + lane] = M[lane];
+            fence_proxy_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(bar(B_PFULL + slot));
+                mbar_arrive(bar(B_TOKEMPTY + slot));
             }
+        };
+        auto epilogue = [&](int i) {
+            const int slot = i & 1;
+            const uint32_t use = (uint32_t)((i >> 1) & 1);
+            mbar_wait(bar(B_OFULL + slot), use);
+            tc_fence_after();
+            uint32_t r[16];
+            tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + o_col(slot), r);
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(B_OEMPTY + slot));
+            const Item it = item(i);
+            const int b = it.row / Hkv, h = it.row % Hkv;
+            const int d = quad * 32 + lane;
 #pragma unroll
             for (int g = 0; g < G; g++) {
-                const float pj = __shfl_sync(0xffffffffu, pw[g], j);
+                float *dst = partials + (((size_t)b * Hq + h * G + g) * n_splits + it.chunk) * (D + 2);
+                if (d < D) dst[2 + d] = __fadd_rn(__uint_as_float(r[g]), __uint_as_float(r[G + g]));
+                if (d == 0) {
+                    float L = 0.0f;
 #pragma unroll
-                for (int i = 0; i < DL; i++) o[g][i] = fmaf(pj, vv[i], o[g][i]);
+                    for (int w = 0; w < 4; w++) L += s_wsum[(slot * 4 + w) * 8 + g];
+                    dst[0] = s_mrow[slot * 8 + g];
+                    dst[1] = L;
+                }
             }
+        };
+        if (n_items > 0) softmax(0);
+        for (int i = 0; i < n_items; i++) {
+            if (i + 1 < n_items) softmax(i + 1);
+            epilogue(i);
         }
     }
-    // merge the 4 warps (fixed order)
-    if (lane == 0) {
-#pragma unroll
-        for (int g = 0; g < G; g++) { wm[warp][g] = m[g]; wl[warp][g] = l[g]; }
-    }
-#pragma unroll
-    for (int g = 0; g < G; g++)
-#pragma unroll
-        for (int i = 0; i < DL; i++) wo[warp][g][lane * DL + i] = o[g][i];
+    tc_fence_before();
     __syncthreads();
-    float *dst_base = partials;
-    for (int idx = threadIdx.x; idx < G * D; idx += kThreads) {
-        const int g = idx / D, d = idx % D;
-        float M = -INFINITY;
-        for (int w = 0; w < kWarps; w++) M = fmaxf(M, wm[w][g]);
-        float L = 0.0f, O = 0.0f;
-        if (M != -INFINITY) {
-            for (int w = 0; w < kWarps; w++) {
-                const float a = exp2f(wm[w][g] - M);
-                L = fmaf(wl[w][g], a, L);
-                O = fmaf(wo[w][g][d], a, O);
-            }
-        }
-        const int hq = h * G + g;
-        float *dst = dst_base + (((size_t)b * Hq + hq) * n_splits + split) * (D + 2);
-        dst[2 + d] = O;
-        if (d == 0) { dst[0] = M; dst[1] = L; }
-    }
+    if (warp == kMmaWarp) tmem_dealloc<128>(tmem_base);
 }
 
 template <int D>
@@ -199,10 +448,16 @@ template <int D, int G>
 cudaError_t launch(const asp_decode_params &p, const asp_bf16 *q, const asp_bf16 *k,
                    const asp_bf16 *v, const int32_t *seq_lens, const int32_t *idx, float *out,
                    float *partials, cudaStream_t s) {
+    using C = DCfg<D>;
     const int ns = n_splits_of(p);
-    dim3 grid(ns, p.n_kv_heads, p.batch);
-    decode_partial_kernel<D, G><<<grid, kThreads, 0, s>>>(p, q, k, v, seq_lens, idx, partials, ns);
-    cudaError_t e = cudaGetLastError();
+    const long total = (long)p.batch * p.n_kv_heads * ns;
+    const int grid = (int)(total < asp_sm_count() ? total : asp_sm_count());
+    cudaError_t e = cudaFuncSetAttribute(decode_tc_kernel<D, G>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    decode_tc_kernel<D, G><<<grid, kThreads, C::kSmemBytes, s>>>(p, q, k, v, seq_lens, idx,
+                                                                 partials, ns);
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     decode_combine_kernel<D><<<dim3(p.n_q_heads, p.batch), D, 0, s>>>(p, partials, out, ns);
     return cudaGetLastError();

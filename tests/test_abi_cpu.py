@@ -99,7 +99,7 @@ def test_score_select_validation_and_workspace(L):
 
 def _dec(**kw):
     d = dict(batch=2, n_q_heads=32, n_kv_heads=8, head_dim=128, top_k=64, n_fresh=1,
-             sm_scale=128 ** -0.5, k_stride_b=8 * 1024 * 128, k_stride_h=1024 * 128,
+             max_seq_len=1024, sm_scale=128 ** -0.5, k_stride_b=8 * 1024 * 128, k_stride_h=1024 * 128,
              k_stride_t=128, v_stride_b=8 * 1024 * 128, v_stride_h=1024 * 128, v_stride_t=128)
     d.update(kw)
     return asp.DecodeParams(*[d[f] for f, _ in asp.DecodeParams._fields_])
@@ -122,6 +122,8 @@ def test_sparse_decode_validation_and_workspace(L):
     assert call(_dec(head_dim=80, k_stride_t=80, v_stride_t=80)) == 3
     assert call(_dec(v_stride_h=1004)) == 1
     assert call(_dec(sm_scale=float("nan"))) == 1
+    assert call(_dec(max_seq_len=0)) == 2
+    assert call(_dec(k_stride_h=1024 * 128 + 8)) == 3           # not a multiple of stride_t
 
 
 def test_synth_library_exports():

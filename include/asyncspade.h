@@ -141,7 +141,10 @@ ASP_API asp_status asyncspade_predict_query(const asp_predict_params *p, const f
  *
  * q_hat     device fp32 [batch][n_q_heads][head_dim].
  * k_cache   device bf16; element (b,h,n,d) at
- *           b*k_stride_b + h*k_stride_h + n*k_stride_t + d (d-stride 1).
+ *           b*k_stride_b + h*k_stride_h + n*k_stride_t + d (d-stride 1);
+ *           k_stride_b and k_stride_h must be multiples of k_stride_t (the
+ *           kernel streams the cache as TMA tiles of a [rows][head_dim]
+ *           view), else ASP_ERR_UNSUPPORTED.
  * seq_lens  device int32 [batch], 0 <= seq_lens[b] <= max_seq_len.
  * sel_idx   device int32 [batch][n_kv_heads][top_k], written.  A row with
  *           seq_lens[b] < top_k holds all its tokens then -1 padding and

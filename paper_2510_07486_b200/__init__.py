@@ -71,11 +71,14 @@ def lib() -> ctypes.CDLL:
     """Load libasyncspade.so (raises if it was not built: no fallback)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
+        # ASYNCSPADE_LIB selects an instrumented build of the same library
+        # (scripts/, development only); the default is the in-tree product.
+        path = os.environ.get("ASYNCSPADE_LIB", LIB_PATH)
+        if not os.path.exists(path):
             raise AsyncSpadeError(
-                f"{LIB_PATH} missing: run `python -m paper_2510_07486_b200.build` "
+                f"{path} missing: run `python -m paper_2510_07486_b200.build` "
                 "(there is no CPU fallback)")
-        L = ctypes.CDLL(LIB_PATH)
+        L = ctypes.CDLL(path)
         vp, sz = ctypes.c_void_p, ctypes.c_size_t
         L.asyncspade_predict_query.argtypes = [ctypes.POINTER(PredictParams), vp, vp, vp, vp]
         L.asyncspade_predict_query.restype = ctypes.c_int32

@@ -77,6 +77,21 @@ def build(verbose: bool = False) -> list[str]:
     return [LIB, SYNTH_LIB]
 
 
+def build_profiling(defines: list[str]) -> str:
+    """Instrumented variant (e.g. -DASP_PROFILE_SCORE) at build/prof/ -- dev only."""
+    out_dir = os.path.join(BUILD, "prof")
+    os.makedirs(out_dir, exist_ok=True)
+    objs = []
+    for f in PRODUCT_SOURCES:
+        obj = os.path.join(out_dir, f + ".o")
+        cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, *defines, "-c", os.path.join(CSRC, f), "-o", obj]
+        subprocess.run(cmd, check=True, capture_output=True)
+        objs.append(obj)
+    out = os.path.join(out_dir, "libasyncspade_prof.so")
+    subprocess.run([_nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", out, *objs], check=True)
+    return out
+
+
 if __name__ == "__main__":
     import sys
     for p in build(verbose="-v" in sys.argv):

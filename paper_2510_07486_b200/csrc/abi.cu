@@ -24,6 +24,8 @@ asp_status check_select(const asp_select_params *p) {
     if (p->aggregation != ASP_AGG_MAX && p->aggregation != ASP_AGG_SUM) return ASP_ERR_INVALID_ARGUMENT;
     if (p->k_stride_t < p->head_dim || p->k_stride_b < 0 || p->k_stride_h < 0) return ASP_ERR_SHAPE;
     if ((p->k_stride_b | p->k_stride_h | p->k_stride_t) & 7) return ASP_ERR_INVALID_ARGUMENT;
+    // TMA views the cache as [rows][head_dim] with row stride k_stride_t
+    if (p->k_stride_b % p->k_stride_t || p->k_stride_h % p->k_stride_t) return ASP_ERR_UNSUPPORTED;
     return ASP_OK;
 }
 

@@ -21,8 +21,9 @@
 //     with TMA (4-D tensor map over the strided cache, 128-B swizzle,
 //     L2 evict-first) into a 6-stage mbarrier ring; warp 1 owns TMEM and
 //     issues the MMAs (single thread); warp 2 builds the swizzled bf16 B
-//     operand for each new row into a 2-slot ring; warps 4-7 drain TMEM
-//     (tcgen05.ld, 4 accumulator stages) and store the fp32 scores.
+//     operand for each new row into a 2-slot ring; warps 4-11 (two
+//     warpgroups alternating tiles) drain TMEM (tcgen05.ld, 6 accumulator
+//     stages) and store the fp32 scores.
 //
 // Every token's score is a fixed function of its key row and q_hat (the same
 // MMA datapath and the same 3-term epilogue order wherever the tile falls),
@@ -33,15 +34,30 @@
 #include "common.cuh"
 #include "tc.cuh"
 
+#ifdef ASP_PROFILE_SCORE
+__device__ unsigned long long g_score_prof[8];
+#define PWAIT(acc, call)                       \
+    do {                                       \
+        const long long _t0 = clock64();       \
+        call;                                  \
+        acc += clock64() - _t0;                \
+    } while (0)
+#define PFLUSH(idx, acc) atomicAdd(&g_score_prof[idx], (unsigned long long)(acc))
+#else
+#define PWAIT(acc, call) call
+#define PFLUSH(idx, acc) (void)(acc)
+#endif
+
 namespace {
 
 using namespace asp::tc;
 
 constexpr int kTileM = 128;           // tokens per tile (MMA M)
 constexpr int kStages = 6;            // K-tile ring depth
-constexpr int kAcc = 4;               // TMEM accumulator stages
+constexpr int kAcc = 6;               // TMEM accumulator stages
+constexpr int kGroup = 3;             // tiles whose MMA chains are interleaved
 constexpr int kBSlots = 2;            // B-operand ring
-constexpr int kThreads = 256;         // 8 warps
+constexpr int kThreads = 384;         // 12 warps: TMA, MMA, B build, spare, 2 x 4 epilogue
 
 template <int D, int G>
 struct Cfg {
@@ -50,8 +66,8 @@ struct Cfg {
     static constexpr int kStageBytes = kTileM * D * 2;
     static constexpr int kBRegionBytes = N * 128;
     static constexpr int kBSlotBytes = kRegions * kBRegionBytes;
-    static constexpr uint32_t kTmemCols = (kAcc * N) <= 32 ? 32 : (kAcc * N) <= 64 ? 64
-                                          : (kAcc * N) <= 128 ? 128 : 256;
+    static constexpr uint32_t kTmemCols = (2 * kAcc * N) <= 64 ? 64 : (2 * kAcc * N) <= 128 ? 128
+                                          : (2 * kAcc * N) <= 256 ? 256 : 512;
     static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes +
                                       kBSlots * kBSlotBytes + 256 /*barriers*/;
 };
@@ -61,16 +77,36 @@ struct TileIter {
     int tpr, n_kv;
     const int32_t *seq_lens;
     int max_len;
-    __device__ int len_of(int row) const {
-        return min(max(seq_lens[row / n_kv], 0), max_len);
-    }
-    // advance i to the next valid tile (token base < row length) in [i, end)
-    __device__ long next(long i) const {
-        while (i < end) {
-            const int row = (int)(i / tpr), j = (int)(i % tpr);
-            if (j * kTileM < len_of(row)) return i;
-            i = (long)(row + 1) * tpr;             // rest of the row is past its length
+    int crow = -1, clen = 0;                       // per-thread cache of the current row's length
+    __device__ int len_of(int row) {
+        if (row != crow) {                         // rows change rarely: one global load per row
+            crow = row;
+            clen = min(max(seq_lens[row / n_kv], 0), max_len);
         }
+        return clen;
+    }
+    // Advance i to the next valid tile (token base < row length) in [i, end);
+    // row / j of the returned tile are left in row, j.  Sequential calls
+    // (i = previous + 1) step the cursor without any 64-bit division.
+    long pos = -1;
+    int row = 0, j = 0;
+    __device__ long next(long i) {
+        int r, jj;
+        if (pos >= 0 && i == pos + 1) {
+            r = row;
+            jj = j + 1;
+            if (jj == tpr) { r++; jj = 0; }
+        } else {
+            r = (int)(i / tpr);
+            jj = (int)(i - (long)r * tpr);
+        }
+        while (i < end) {
+            if (jj * kTileM < len_of(r)) { pos = i; row = r; j = jj; return i; }
+            i += tpr - jj;                        // rest of the row is past its length
+            r++;
+            jj = 0;
+        }
+        pos = end;
         return end;
     }
 };
@@ -122,60 +158,92 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder_g;
+#ifdef ASP_PROFILE_SCORE
+    const long long t_kernel0 = clock64();
+#endif
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
+            long long pw_empty = 0;
             for (long i = it.next(it.start); i < it.end; i = it.next(i + 1)) {
-                const int row = (int)(i / it.tpr), j = (int)(i % it.tpr);
+                const int row = it.row, j = it.j;
                 const int b = row / p.n_kv_heads, h = row % p.n_kv_heads;
-                mbar_wait(empty_bar(s), ph ^ 1);
+                const int grow = (int)((b * p.k_stride_b + h * p.k_stride_h) / p.k_stride_t) +
+                                 j * kTileM;
+                PWAIT(pw_empty, mbar_wait(empty_bar(s), ph ^ 1));
                 mbar_arrive_expect_tx(full_bar(s), C::kStageBytes);
                 const uint32_t dst = stage0 + s * C::kStageBytes;
 #pragma unroll
                 for (int r = 0; r < C::kRegions; r++)
-                    tma_load_4d(dst + r * (kTileM * 128), &kmap, full_bar(s), r * 64, j * kTileM,
-                                h, b, kEvictFirst);
+                    tma_load_2d(dst + r * (kTileM * 128), &kmap, full_bar(s), r * 64, grow,
+                                kEvictFirst);
                 if (++s == kStages) { s = 0; ph ^= 1; }
             }
+            PFLUSH(0, pw_empty);
         }
         __syncwarp();
     } else if (warp == 1) {
-        // ------------------------------------------------ MMA issuer (one thread)
-        if (lane == 0) {
+        // ------------------------------------------------ MMA issuer (whole warp, one elected lane)
+        // A tile's D/16 MMAs are a dependent accumulation chain and each MMA is far
+        // shorter than the tensor pipe's latency, so chains are interleaved: every
+        // tile accumulates into two TMEM halves (even / odd k-steps) and tiles are
+        // issued in groups of up to kGroup (same row), k-step outer / tile inner
+        // -- 2 x kGroup independent chains in flight.
+        {
             constexpr uint32_t idesc = idesc_bf16_f32(kTileM, N);
             int s = 0, a = 0, bs = -1;
             uint32_t ph = 0, aph = 0, bph = 0;
             int cur_row = -1;
-            for (long i = it.next(it.start); i < it.end; i = it.next(i + 1)) {
-                const int row = (int)(i / it.tpr);
+            long long pm_full = 0, pm_tempty = 0, pm_issue = 0, pm_b = 0;
+            long i = it.next(it.start);
+            while (i < it.end) {
+                const int row = it.row;
                 if (row != cur_row) {
-                    if (bs >= 0) mma_commit(bempty_bar(bs));        // previous row's B slot free
+                    if (bs >= 0) mma_commit_warp(bempty_bar(bs));   // previous row's B slot free
                     bs = (bs + 1) % kBSlots;
                     if (bs == 0 && cur_row != -1) bph ^= 1;
-                    mbar_wait(bfull_bar(bs), bph);
+                    PWAIT(pm_b, mbar_wait(bfull_bar(bs), bph));
                     cur_row = row;
                 }
-                mbar_wait(full_bar(s), ph);
-                mbar_wait(tempty_bar(a), aph ^ 1);
+                // collect a group of consecutive valid tiles of this row
+                int gs[kGroup], ga[kGroup], ng = 0;
+                while (ng < kGroup && i < it.end && it.row == row) {
+                    PWAIT(pm_full, mbar_wait(full_bar(s), ph));
+                    PWAIT(pm_tempty, mbar_wait(tempty_bar(a), aph ^ 1));
+                    gs[ng] = s;
+                    ga[ng] = a;
+                    ng++;
+                    if (++s == kStages) { s = 0; ph ^= 1; }
+                    if (++a == kAcc) { a = 0; aph ^= 1; }
+                    i = it.next(i + 1);
+                }
+#ifdef ASP_PROFILE_SCORE
+                const long long t_issue = clock64();
+#endif
                 tc_fence_after();
-                const uint32_t a_base = stage0 + s * C::kStageBytes;
                 const uint32_t b_base = bslot0 + bs * C::kBSlotBytes;
-                const uint32_t d_tmem = tmem_base + a * N;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; kk++) {
                     const int r = kk / 4, ko = (kk % 4) * 32;
-                    mma_bf16(d_tmem, desc_sw128_kmajor(a_base + r * (kTileM * 128) + ko),
-                             desc_sw128_kmajor(b_base + r * C::kBRegionBytes + ko), idesc,
-                             kk > 0 ? 1u : 0u);
+                    const uint64_t bdesc = desc_sw128_kmajor(b_base + r * C::kBRegionBytes + ko);
+                    for (int t = 0; t < ng; t++)
+                        mma_bf16_warp(tmem_base + ga[t] * (2 * N) + (kk & 1) * N,
+                                      desc_sw128_kmajor(stage0 + gs[t] * C::kStageBytes +
+                                                        r * (kTileM * 128) + ko),
+                                      bdesc, idesc, kk > 1 ? 1u : 0u);
                 }
-                mma_commit(empty_bar(s));
-                mma_commit(tfull_bar(a));
-                if (++s == kStages) { s = 0; ph ^= 1; }
-                if (++a == kAcc) { a = 0; aph ^= 1; }
+                for (int t = 0; t < ng; t++) {
+                    mma_commit_warp(empty_bar(gs[t]));
+                    mma_commit_warp(tfull_bar(ga[t]));
+                }
+#ifdef ASP_PROFILE_SCORE
+                pm_issue += clock64() - t_issue;
+#endif
             }
+            PFLUSH(1, pm_full); PFLUSH(2, pm_tempty); PFLUSH(3, pm_issue); PFLUSH(7, pm_b);
         }
         __syncwarp();
     } else if (warp == 2) {
@@ -184,7 +252,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
         uint32_t bph = 0;
         int cur_row = -1;
         for (long i = it.next(it.start); i < it.end; i = it.next(i + 1)) {
-            const int row = (int)(i / it.tpr);
+            const int row = it.row;
             if (row == cur_row) continue;
             cur_row = row;
             bs = (bs + 1) % kBSlots;
@@ -229,33 +297,39 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
         }
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue: TMEM -> scores
+        // two warpgroups alternate tiles (each warp drains its 32-lane quadrant)
         const int quad = warp & 3;                  // TMEM lanes 32*quad .. +31
-        int a = 0;
-        uint32_t aph = 0;
+        const int group = (warp - 4) >> 2;
         bool nonfinite = false;
-        for (long i = it.next(it.start); i < it.end; i = it.next(i + 1)) {
-            const int row = (int)(i / it.tpr), j = (int)(i % it.tpr);
-            mbar_wait(tfull_bar(a), aph);
+        long long pe_full = 0;
+        long k = 0;                                 // index of the tile in this CTA's sequence
+        for (long i = it.next(it.start); i < it.end; i = it.next(i + 1), k++) {
+            if ((k & 1) != group) continue;
+            const int a = (int)(k % kAcc);
+            const uint32_t aph = (uint32_t)((k / kAcc) & 1);
+            const int row = it.row, j = it.j;
+            PWAIT(pe_full, mbar_wait(tfull_bar(a), aph));
             tc_fence_after();
-            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + a * N;
-            float v[N];
+            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + a * (2 * N);
+            float v[N];                                 // even + odd k-step halves (fixed order)
             if constexpr (N == 32) {
-                uint32_t r[32];
-                tmem_ld32(taddr, r);
+                uint32_t r0[32], r1[32];
+                tmem_ld32(taddr, r0);
+                tmem_ld32(taddr + N, r1);
                 tmem_wait_ld();
 #pragma unroll
-                for (int c = 0; c < 32; c++) v[c] = __uint_as_float(r[c]);
+                for (int c = 0; c < 32; c++) v[c] = __fadd_rn(__uint_as_float(r0[c]), __uint_as_float(r1[c]));
             } else {
-                uint32_t r[16];
-                tmem_ld16(taddr, r);
+                uint32_t r0[16], r1[16];
+                tmem_ld16(taddr, r0);
+                tmem_ld16(taddr + N, r1);
                 tmem_wait_ld();
 #pragma unroll
-                for (int c = 0; c < 16; c++) v[c] = __uint_as_float(r[c]);
+                for (int c = 0; c < 16; c++) v[c] = __fadd_rn(__uint_as_float(r0[c]), __uint_as_float(r1[c]));
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty_bar(a));
-            if (++a == kAcc) { a = 0; aph ^= 1; }
             float s = 0.0f;
 #pragma unroll
             for (int g = 0; g < G; g++) {
@@ -270,10 +344,14 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
             }
         }
         if (__any_sync(0xffffffffu, nonfinite) && lane == 0) asp::flag_or(dev_flags, ASP_FLAG_NONFINITE);
+        if (warp == 4 && lane == 0) PFLUSH(4, pe_full);
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem_base);
+#ifdef ASP_PROFILE_SCORE
+    if (threadIdx.x == 0) atomicAdd(&g_score_prof[6], (unsigned long long)(clock64() - t_kernel0));
+#endif
 }
 
 // ---------------------------------------------------------------- host side
@@ -296,14 +374,16 @@ cudaError_t launch(const asp_select_params &p, const float *q_hat, const asp_bf1
     using C = Cfg<D, G>;
     auto encode = get_encode();
     if (!encode) return cudaErrorNotSupported;
+    // 2-D row view [rows][D] of the cache: row(b, h, t) = (b*sb + h*sh)/st + t
+    // (the ABI requires sb, sh to be multiples of st); a tile is 128 rows.
     CUtensorMap map;
-    const cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)p.max_seq_len,
-                                (cuuint64_t)p.n_kv_heads, (cuuint64_t)p.batch};
-    const cuuint64_t strides[3] = {(cuuint64_t)p.k_stride_t * 2, (cuuint64_t)p.k_stride_h * 2,
-                                   (cuuint64_t)p.k_stride_b * 2};
-    const cuuint32_t box[4] = {64, (cuuint32_t)kTileM, 1, 1};
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<asp_bf16 *>(k), dims,
+    const int64_t rows = ((int64_t)(p.batch - 1) * p.k_stride_b +
+                          (int64_t)(p.n_kv_heads - 1) * p.k_stride_h) / p.k_stride_t + p.max_seq_len;
+    const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)p.k_stride_t * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)kTileM};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<asp_bf16 *>(k), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -320,6 +400,15 @@ cudaError_t launch(const asp_select_params &p, const float *q_hat, const asp_bf1
 }
 
 }  // namespace
+
+#ifdef ASP_PROFILE_SCORE
+extern "C" __attribute__((visibility("default"))) int asp_score_prof_read(unsigned long long *host) {
+    cudaMemcpyFromSymbol(host, g_score_prof, sizeof(g_score_prof));
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_score_prof, z, sizeof(z));
+    return 0;
+}
+#endif
 
 cudaError_t asp_launch_score(const asp_select_params &p, const float *q_hat,
                              const asp_bf16 *k_cache, const int32_t *seq_lens, float *scores,

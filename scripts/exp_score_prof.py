@@ -1,0 +1,21 @@
+"""Run score_select with the instrumented library and print the cycle budget."""
+import ctypes, os, sys, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["ASYNCSPADE_LIB"] = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build/prof/libasyncspade_prof.so")
+import paper_2510_07486_b200 as asp
+from paper_2510_07486_b200 import configs
+from paper_2510_07486_b200.step import DecodeStep
+step = DecodeStep(configs.QWEN3_32B, "cuda")
+step.fill_synthetic()
+asp.predict_query(step.window, step.q_hat, params=step.p_pred)
+L = asp.lib()
+buf = (ctypes.c_ulonglong * 8)()
+for it in range(3):
+    L.asp_score_prof_read(buf)
+    asp.score_select(step.q_hat, step.k_cache, step.seq_lens, 2048, sel_idx=step.sel_idx, workspace=step.ws_sel, params=step.p_sel)
+    torch.cuda.synchronize()
+L.asp_score_prof_read(buf)
+names = ["prod_wait_empty", "mma_wait_full", "mma_wait_tempty", "mma_issue", "epi_wait_tfull", "-", "cta_total", "mma_wait_bfull"]
+ctas = 148
+for n, v in zip(names, buf):
+    print(f"{n:18s} {v / ctas / 1.93e3:9.1f} us/CTA")

@@ -94,6 +94,7 @@ def test_score_select_validation_and_workspace(L):
     assert call(_sel(aggregation=2)) == 1
     assert call(_sel(k_stride_t=100)) == 2                     # shorter than a row
     assert call(_sel(k_stride_t=132)) == 1                     # not a multiple of 8 elements
+    assert call(_sel(k_stride_h=1024 * 128 + 8)) == 3          # not a multiple of k_stride_t
     assert L.asyncspade_score_select_workspace(ctypes.byref(_sel(batch=0))) == 0
 
 

@@ -106,9 +106,9 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
     const long i_start = total * blockIdx.x / gridDim.x;
     const long i_end = total * (blockIdx.x + 1) / gridDim.x;
     const int n_items = (int)(i_end - i_start);
-    auto item = [&](int i) -> Item {
-        const long g = i_start + i;
-        return Item{(int)(g / n_splits), (int)(g % n_splits)};
+    auto item = [&](int i) -> Item {               // total items < 2^31: 32-bit math
+        const int g = (int)i_start + i;
+        return Item{g / n_splits, g % n_splits};
     };
 
     if (threadIdx.x == 0) {
@@ -234,7 +234,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
         asm volatile("cp.async.wait_all;" ::: "memory");
     } else if (warp == kMmaWarp) {
         // ================================================= MMA issuer
-        if (lane == 0) {
+        {                                   // whole warp; one elected lane issues
             constexpr uint32_t idesc1 = idesc_bf16_f32(kTile, kN);                 // K-major A, B
             constexpr uint32_t idesc2 = idesc_bf16_f32(kTile, kN) | (1u << 15);    // A MN-major
             int s = 0, qs = -1, cur_row = -1;
@@ -248,7 +248,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                 const int slot = i & 1;
                 const Item it = item(i);
                 if (it.row != cur_row) {
-                    if (qs >= 0) mma_commit(bar(B_QEMPTY + qs));
+                    if (qs >= 0) mma_commit_warp(bar(B_QEMPTY + qs));
                     qs = (qs + 1) & 1;
                     if (qs == 0 && cur_row != -1) qph ^= 1;
                     mbar_wait(bar(B_QFULL + qs), qph);
@@ -261,14 +261,14 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
 #pragma unroll
                     for (int kk = 0; kk < D / 16; kk++) {
                         const int r = kk / 4, ko = (kk % 4) * 32;
-                        mma_bf16(tmem_base + s_col(slot, t),
+                        mma_bf16_warp(tmem_base + s_col(slot, t),
                                  desc_sw128_kmajor(ab + r * (kTile * 128) + ko),
                                  desc_sw128_kmajor(qb + r * (kN * 128) + ko), idesc1, kk > 0 ? 1u : 0u);
                     }
-                    mma_commit(bar(B_EMPTY + s));
+                    mma_commit_warp(bar(B_EMPTY + s));
                     if (++s == C::kStages) { s = 0; ph ^= 1; }
                 }
-                mma_commit(bar(B_SFULL + slot));
+                mma_commit_warp(bar(B_SFULL + slot));
             };
             auto mma2 = [&](int i) {
                 const int slot = i & 1;
@@ -289,12 +289,12 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                         ad = (ad & ~(0x3FFFull << 16)) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16);
                         const uint64_t bd = desc_sw128_kmajor(pb + t * C::kPTileBytes +
                                                               (kk / 4) * (kN * 128) + (kk % 4) * 32);
-                        mma_bf16(tmem_base + o_col(slot), ad, bd, idesc2, (t | kk) ? 1u : 0u);
+                        mma_bf16_warp(tmem_base + o_col(slot), ad, bd, idesc2, (t | kk) ? 1u : 0u);
                     }
-                    mma_commit(bar(B_EMPTY + s));
+                    mma_commit_warp(bar(B_EMPTY + s));
                     if (++s == C::kStages) { s = 0; ph ^= 1; }
                 }
-                mma_commit(bar(B_OFULL + slot));
+                mma_commit_warp(bar(B_OFULL + slot));
             };
             if (n_items > 0) mma1(0);
             for (int i = 0; i < n_items; i++) {

@@ -213,10 +213,9 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if cfg.n_kv_heads % world:
-        raise SystemExit("KV heads must divide evenly over ranks")
-    hn = cfg.n_kv_heads // world
-    step = DecodeStep(cfg, "cuda", kv_heads=(rank * hn, hn))
+    from paper_2510_07486_b200.shard import kv_head_shard
+    h0, hn = kv_head_shard(cfg.n_kv_heads, world, rank)     # §8(e): KV-head sharding
+    step = DecodeStep(cfg, "cuda", kv_heads=(h0, hn))
     step.fill_synthetic()
     torch.cuda.synchronize()
 

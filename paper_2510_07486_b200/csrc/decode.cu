@@ -10,16 +10,19 @@
 // the chunk partials merged in chunk order by a small combine kernel.  Each
 // chunk is one work item of a persistent, warp-specialised kernel:
 //
-//   warp 0   TMA producer: resolves the chunk's token list and GATHERS the
-//            selected key / value rows straight into 128-B-swizzled shared
-//            memory with cp.async.bulk.tensor tile::gather4 (4 rows per
-//            instruction, one per lane), 128-token tiles, 5-stage ring;
-//   warp 1   TMEM owner + single-thread tcgen05.mma issuer:
+//   warps 0-3  producers: resolve the chunk's token list (indices fetched one
+//            item ahead), build the bf16 Q operand when the row changes, and
+//            GATHER the selected key / value rows with cp.async (16 lanes per
+//            256-B row, coalesced) straight into the 128-B-swizzled UMMA
+//            layout; 128-token tiles in a 5-stage ring; each producer waits
+//            its copies two tiles later, fences them to the async proxy and
+//            arrives on the stage's mbarrier.  (TMA tile::gather4 was measured
+//            ~2.5x slower for 256-B random rows.)
+//   warp 8   TMEM owner + tcgen05.mma issuer (warp-uniform, one elected lane):
 //              S^T[128 tok x 16] = K_tile . Q^T          (q is bf16: exact)
 //              O^T[D x 16]      += V_tile^T . P^T        (V tile MN-major)
 //            P = [p_hi; p_lo] is the fp32 softmax weight split into two bf16
 //            terms (rel. error 2^-17), so the P.V products stay fp32-exact;
-//   warp 2   builds the bf16 Q operand when the row changes;
 //   warps 4-7  softmax (chunk max / exp2 / sums with warp shuffles and one
 //            named barrier) writing the P operand, then the epilogue that
 //            drains O from TMEM and stores the chunk partial (m, l, o).
@@ -29,6 +32,19 @@
 // gather stream (537 MB of K/V rows at the Qwen3-32B shape).
 #include "common.cuh"
 #include "tc.cuh"
+
+#ifdef ASP_PROFILE_DECODE
+__device__ unsigned long long g_dec_prof[16];
+#define DWAIT(idx, call)                                                                 \
+    do {                                                                                 \
+        const long long _t0 = clock64();                                                 \
+        call;                                                                            \
+        if (threadIdx.x == 0 || threadIdx.x == kMmaWarp * 32 || threadIdx.x == 128)       \
+            atomicAdd(&g_dec_prof[idx], (unsigned long long)(clock64() - _t0));          \
+    } while (0)
+#else
+#define DWAIT(idx, call) call
+#endif
 
 namespace {
 
@@ -137,6 +153,9 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder_g;
+#ifdef ASP_PROFILE_DECODE
+    const long long t_k0 = clock64();
+#endif
     // TMEM columns: S[slot][tile] at slot*32 + tile*16, O[slot] at 64 + slot*16
     auto s_col = [](int slot, int t) { return (uint32_t)(slot * 32 + t * 16); };
     auto o_col = [](int slot) { return (uint32_t)(64 + slot * 16); };
@@ -150,6 +169,32 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
         const int pt = threadIdx.x;                           // 0..127
         int s = 0, qs = -1, cur_row = -1;
         uint32_t ph = 0, qph = 0;
+        // software pipeline: the selection indices and row length of the NEXT item
+        // are loaded while the current one is being gathered
+        constexpr int kEntriesPerThread = kChunk / kProducerThreads;
+        int pre_raw[kEntriesPerThread] = {0, 0};
+        int pre_len = 0;
+        auto fetch = [&](int i) {
+            const Item it = item(i);
+            pre_len = seq_lens[it.row / Hkv];
+            const int32_t *ib = sel_idx + (size_t)it.row * p.top_k;
+#pragma unroll
+            for (int u = 0; u < kEntriesPerThread; u++) {
+                const int e = it.chunk * kChunk + pt + u * kProducerThreads;
+                pre_raw[u] = e < p.top_k ? __ldg(ib + e) : -1;
+            }
+        };
+        if (n_items > 0) fetch(0);
+        constexpr int kLag = 2;                               // < kStages
+        int pending[kLag + 1];
+        int npend = 0;
+        auto release_oldest = [&]() {
+            asm volatile("cp.async.wait_group %0;" ::"n"(kLag) : "memory");
+            fence_proxy_async_smem();
+            mbar_arrive(bar(B_FULL + pending[0]));
+            for (int u = 1; u < npend; u++) pending[u - 1] = pending[u];
+            npend--;
+        };
         auto prepare = [&](int i) {
             const int slot = i & 1;
             const Item it = item(i);
@@ -159,7 +204,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                 qs = (qs + 1) & 1;
                 if (qs == 0 && cur_row != -1) qph ^= 1;
                 cur_row = it.row;
-                mbar_wait(bar(B_QEMPTY + qs), qph ^ 1);
+                DWAIT(0, mbar_wait(bar(B_QEMPTY + qs), qph ^ 1));
                 const asp_bf16 *qsrc = q + ((size_t)b * Hq + (size_t)h * G) * D;
                 unsigned char *qslot = gb + (qslot0 - base) + qs * C::kQSlotBytes;
                 for (int c = pt; c < kN * D / 8; c += kProducerThreads) {
@@ -172,15 +217,22 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                 }
                 fence_proxy_async_smem();
             }
-            mbar_wait(bar(B_TOKEMPTY + slot), ((i >> 1) & 1) ^ 1);
-            const int len = min(max(seq_lens[b], 0), p.max_seq_len);
+            // this item's indices were fetched one item ahead (pre_*); fetch the next
+            const int len = min(max(pre_len, 0), p.max_seq_len);
+            const int raw[kEntriesPerThread] = {pre_raw[0], pre_raw[1]};
+            if (i + 1 < n_items) fetch(i + 1);
+            DWAIT(1, mbar_wait(bar(B_TOKEMPTY + slot), ((i >> 1) & 1) ^ 1));
+            // WAR: every producer thread must be done reading this slot for the
+            // previous item's V gather before anyone overwrites it
+            asm volatile("bar.sync 2, %0;" ::"n"(kProducerThreads) : "memory");
             const int fresh_lo = max(len - p.n_fresh, 0);
-            const int32_t *ib = sel_idx + (size_t)it.row * p.top_k;
-            for (int j = pt; j < kChunk; j += kProducerThreads) {
+#pragma unroll
+            for (int u = 0; u < kEntriesPerThread; u++) {
+                const int j = pt + u * kProducerThreads;
                 const int e = it.chunk * kChunk + j;
                 int tok = -1;
                 if (e < p.top_k) {
-                    const int t = ib[e];
+                    const int t = raw[u];
                     if (t >= 0 && t < fresh_lo) tok = t;
                 } else if (e < E) {
                     const int t = fresh_lo + (e - p.top_k);
@@ -204,7 +256,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             const int chunk = pt % kChunksPerRow;
             const int region = chunk / 8, cc = chunk % 8;
             for (int t = 0; t < kTilesPerItem; t++) {
-                mbar_wait(bar(B_EMPTY + s), ph ^ 1);
+                DWAIT(2, mbar_wait(bar(B_EMPTY + s), ph ^ 1));
                 const uint32_t stage = stage0 + s * C::kStageBytes + region * (kTile * 128);
                 const int32_t *tk = s_tok + slot * kChunk + t * kTile;
 #pragma unroll 4
@@ -215,8 +267,12 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src)
                                  : "memory");
                 }
-                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar(B_FULL + s))
-                             : "memory");
+                // cp.async writes are generic-proxy: each producer waits for its group
+                // from kLag tiles ago, fences it to the async proxy (tensor core), and
+                // only then arrives -- kLag + 1 tiles of copies stay in flight per thread
+                asm volatile("cp.async.commit_group;" ::: "memory");
+                pending[npend++] = s;
+                if (npend > kLag) release_oldest();
                 if (++s == C::kStages) { s = 0; ph ^= 1; }
             }
         };
@@ -231,7 +287,9 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             }
             load(i, v_cache, p.v_stride_b, p.v_stride_h, p.v_stride_t);
         }
-        asm volatile("cp.async.wait_all;" ::: "memory");
+        asm volatile("cp.async.wait_all;" ::: "memory");   // drain the lagged stages
+        fence_proxy_async_smem();
+        for (int u = 0; u < npend; u++) mbar_arrive(bar(B_FULL + pending[u]));
     } else if (warp == kMmaWarp) {
         // ================================================= MMA issuer
         {                                   // whole warp; one elected lane issues
@@ -240,7 +298,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             int s = 0, qs = -1, cur_row = -1;
             uint32_t ph = 0, qph = 0;
             auto wait_stage = [&]() {
-                mbar_wait(bar(B_FULL + s), ph);
+                DWAIT(3, mbar_wait(bar(B_FULL + s), ph));
                 fence_proxy_async_smem();        // cp.async (generic proxy) -> tensor core reads
                 tc_fence_after();
             };
@@ -251,7 +309,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                     if (qs >= 0) mma_commit_warp(bar(B_QEMPTY + qs));
                     qs = (qs + 1) & 1;
                     if (qs == 0 && cur_row != -1) qph ^= 1;
-                    mbar_wait(bar(B_QFULL + qs), qph);
+                    DWAIT(4, mbar_wait(bar(B_QFULL + qs), qph));
                     cur_row = it.row;
                 }
                 const uint32_t qb = qslot0 + qs * C::kQSlotBytes;
@@ -273,8 +331,8 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             auto mma2 = [&](int i) {
                 const int slot = i & 1;
                 const uint32_t use = (uint32_t)((i >> 1) & 1);
-                mbar_wait(bar(B_PFULL + slot), use);
-                mbar_wait(bar(B_OEMPTY + slot), use ^ 1);
+                DWAIT(5, mbar_wait(bar(B_PFULL + slot), use));
+                DWAIT(6, mbar_wait(bar(B_OEMPTY + slot), use ^ 1));
                 tc_fence_after();
                 const uint32_t pb = pslot0 + slot * C::kPSlotBytes;
                 for (int t = 0; t < kTilesPerItem; t++) {
@@ -310,8 +368,8 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
         auto softmax = [&](int i) {
             const int slot = i & 1;
             const uint32_t use = (uint32_t)((i >> 1) & 1);
-            mbar_wait(bar(B_TOKFULL + slot), use);
-            mbar_wait(bar(B_SFULL + slot), use);
+            DWAIT(7, mbar_wait(bar(B_TOKFULL + slot), use));
+            DWAIT(8, mbar_wait(bar(B_SFULL + slot), use));
             tc_fence_after();
             float l[kTilesPerItem][G];
             int tok[kTilesPerItem];
@@ -324,6 +382,24 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
 #pragma unroll
                 for (int g = 0; g < G; g++)
                     l[t][g] = tok[t] >= 0 ? __uint_as_float(r[g]) * scale : -INFINITY;
+#ifdef ASP_DEBUG_DECODE
+                if (tok[t] >= 0) {               // recompute S on CUDA cores from global K
+                    const Item itd = item(i);
+                    const int bd = itd.row / Hkv, hd = itd.row % Hkv;
+                    const asp_bf16 *kr = k_cache + bd * p.k_stride_b + hd * p.k_stride_h +
+                                         (int64_t)tok[t] * p.k_stride_t;
+                    const asp_bf16 *qr = q + ((size_t)bd * Hq + (size_t)hd * G) * D;
+#pragma unroll
+                    for (int g = 0; g < G; g++) {
+                        float acc = 0.f;
+                        for (int d = 0; d < D; d++)
+                            acc += asp::bf16f(qr[g * D + d]) * asp::bf16f(kr[d]);
+                        if (fabsf(acc - __uint_as_float(r[g])) > 1e-3f * (1.f + fabsf(acc)))
+                            atomicAdd(&g_dec_prof[12], 1ull);
+                    }
+                    atomicAdd(&g_dec_prof[13], 1ull);
+                }
+#endif
             }
             float mx[G];
 #pragma unroll
@@ -384,7 +460,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
         auto epilogue = [&](int i) {
             const int slot = i & 1;
             const uint32_t use = (uint32_t)((i >> 1) & 1);
-            mbar_wait(bar(B_OFULL + slot), use);
+            DWAIT(9, mbar_wait(bar(B_OFULL + slot), use));
             tc_fence_after();
             uint32_t r[16];
             tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + o_col(slot), r);
@@ -417,6 +493,9 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
     tc_fence_before();
     __syncthreads();
     if (warp == kMmaWarp) tmem_dealloc<128>(tmem_base);
+#ifdef ASP_PROFILE_DECODE
+    if (threadIdx.x == 0) atomicAdd(&g_dec_prof[10], (unsigned long long)(clock64() - t_k0));
+#endif
 }
 
 template <int D>
@@ -464,6 +543,15 @@ cudaError_t launch(const asp_decode_params &p, const asp_bf16 *q, const asp_bf16
 }
 
 }  // namespace
+
+#ifdef ASP_PROFILE_DECODE
+extern "C" __attribute__((visibility("default"))) int asp_decode_prof_read(unsigned long long *host) {
+    cudaMemcpyFromSymbol(host, g_dec_prof, sizeof(g_dec_prof));
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_dec_prof, z, sizeof(z));
+    return 0;
+}
+#endif
 
 size_t asp_decode_partials_bytes(const asp_decode_params &p) {
     return (size_t)p.batch * p.n_q_heads * n_splits_of(p) * (p.head_dim + 2) * sizeof(float);

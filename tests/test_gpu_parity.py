@@ -324,3 +324,21 @@ def test_step_with_fresh_token():
         V = synth.kv_rows(seed, synth.STREAM_V, b, h, 0, L, cfg.n_kv_heads, L, D)[None, None]
         o_or = oracle.sparse_decode(q, K, V, idx_g[b:b + 1, h:h + 1], [L], 1)
         assert rel_inf_err(out_g[b, h * G:(h + 1) * G], o_or[0]) <= ATTN_RTOL
+
+
+def test_decode_independent_of_cache_state():
+    """Regression: the decode result must not depend on timing (a producer
+    WAR race on the token list once showed up only with a cold L2)."""
+    cfg = configs.QWEN3_8B.with_(batch=8, seq_len=16384, top_k=1024)
+    step = DecodeStep(cfg, DEV)
+    step.fill_synthetic()
+    step.run()
+    torch.cuda.synchronize()
+    ref = step.out.clone()
+    junk = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=DEV)
+    for it in range(3):
+        junk.fill_(it)                                     # evict L2
+        asp.sparse_decode(step.q, step.k_cache, step.v_cache, step.seq_lens, step.sel_idx,
+                          out=step.out, workspace=step.ws_dec, params=step.p_dec)
+        torch.cuda.synchronize()
+        assert torch.equal(step.out, ref)

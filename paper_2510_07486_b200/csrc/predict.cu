@@ -120,25 +120,31 @@ __device__ double ridge_solve(const WarpSmem &s, int W, int h0, int nh, float ep
     __syncwarp();
     if (lane < nh) A[lane * nh + lane] += e;
     __syncwarp();
-    // Cholesky G = L L^T, lane-parallel over rows below the pivot.
+    // Right-looking Cholesky G = L L^T: per pivot, scale the column (lanes over
+    // rows) and apply the rank-1 update to the trailing lower triangle (lanes
+    // over its elements) -- constant dependency depth per column.
     double inv_d_lane = 0.0;
     ok = true;
     for (int j = 0; j < nh; j++) {
-        double sjj = A[j * nh + j];
-        for (int k = 0; k < j; k++) sjj = fma(-A[j * nh + k], A[j * nh + k], sjj);
-        if (!(sjj > 0.0) || !isfinite(sjj)) { ok = false; break; }   // warp-uniform
-        const double dj = sqrt(sjj);
+        const double ajj = A[j * nh + j];
+        if (!(ajj > 0.0) || !isfinite(ajj)) { ok = false; break; }   // warp-uniform
+        const double dj = sqrt(ajj);
         const double inv = 1.0 / dj;
         if (lane == j) inv_d_lane = inv;
-        const int i = j + 1 + lane;
-        double t = 0.0;
-        if (i < nh) {
-            t = A[i * nh + j];
-            for (int k = 0; k < j; k++) t = fma(-A[i * nh + k], A[j * nh + k], t);
-        }
         __syncwarp();
-        if (i < nh) A[i * nh + j] = t * inv;
         if (lane == 0) A[j * nh + j] = dj;
+        for (int i = j + 1 + lane; i < nh; i += 32) A[i * nh + j] *= inv;
+        __syncwarp();
+        const int m = nh - j - 1;                       // trailing block size
+        for (int u = lane; u < m * (m + 1) / 2; u += 32) {
+            // u -> (ii, kk), kk <= ii, row-major over the lower triangle
+            int ii = (int)((sqrtf(8.0f * u + 1.0f) - 1.0f) * 0.5f);
+            if ((ii + 1) * (ii + 2) / 2 <= u) ii++;
+            if (ii * (ii + 1) / 2 > u) ii--;
+            const int kk = u - ii * (ii + 1) / 2;
+            const int i = j + 1 + ii, k = j + 1 + kk;
+            A[i * nh + k] = fma(-A[i * nh + j], A[k * nh + j], A[i * nh + k]);
+        }
         __syncwarp();
     }
     if (!ok) return 0.0;
@@ -176,7 +182,7 @@ __device__ void masked_shared_coeffs(const WarpSmem &s, int W, int n, double v_l
         if (lane >= o) S += t;
     }
     s.e[lane] = e;
-    s.vec[32 + lane] = S;
+    s.vec[32 + lane] = 1.0 / S;                   // reciprocal prefix sums (lane-parallel)
     const bool tiny = __any_sync(0xffffffffu, lane == 0 && !(S > 1e-280));
     s.vec[lane] = v_lane;
     __syncwarp();
@@ -187,7 +193,7 @@ __device__ void masked_shared_coeffs(const WarpSmem &s, int W, int n, double v_l
             if (mm < 1) continue;
             const double mult = (mm == n) ? 2.0 : 1.0;      // rows j = W-1 and W share n_j = n
             if (!tiny) {
-                acc += mult * s.e[p - W + mm] / s.vec[32 + mm - 1];
+                acc += mult * s.e[p - W + mm] * s.vec[32 + mm - 1];
             } else {
                 // a prefix's exponentials underflowed against the global max
                 double mx = s.vec[0];

@@ -68,6 +68,20 @@ __global__ void query_kernel(uint64_t key, float *window, uint16_t *q, int bs, i
     }
 }
 
+// Synthetic forward (SURVEY §8(d), config [4]): a stand-in for the rest of a
+// decoder layer's work on the main stream -- one streaming read of the
+// layer's bf16 weights (Qwen3-8B: ~193 M params, 386 MB).  Bytes only, no
+// GEMM math: on one GPU the overlap question is about sharing HBM.
+__global__ void forward_kernel(const uint4 *__restrict__ w, long long n16, float *sink) {
+    uint32_t acc = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
+         i += (long long)gridDim.x * blockDim.x) {
+        const uint4 v = __ldcs(w + i);
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (acc == 0x9E3779B9u) sink[0] = 1.0f;                 // keeps the loads alive
+}
+
 }  // namespace
 
 extern "C" {
@@ -83,6 +97,13 @@ __attribute__((visibility("default"))) int asp_synth_query(uint64_t stream_key, 
                     int b0, int h0, int hg, void *stream) {
     query_kernel<<<1024, 256, 0, (cudaStream_t)stream>>>(stream_key, window, q, bs, hs, W, D, b0,
                                                          h0, hg);
+    return (int)cudaGetLastError();
+}
+
+__attribute__((visibility("default"))) int asp_synth_forward(const void *weights, long long bytes, float *sink,
+                                                         int n_sm, void *stream) {
+    forward_kernel<<<n_sm * 4, 512, 0, (cudaStream_t)stream>>>((const uint4 *)weights, bytes / 16,
+                                                                sink);
     return (int)cudaGetLastError();
 }
 

@@ -145,6 +145,8 @@ def _dev_lib():
         L.asp_synth_kv.restype = i
         L.asp_synth_query.argtypes = [u64, vp, vp, i, i, i, i, i, i, i, vp]
         L.asp_synth_query.restype = i
+        L.asp_synth_forward.argtypes = [vp, ll, vp, i, vp]
+        L.asp_synth_forward.restype = i
         _synth_lib = L
     return _synth_lib
 
@@ -178,3 +180,21 @@ def fill_query_device(window, q, seed: int, b0: int = 0, h0: int = 0,
                                     bs, hs, W, D, b0, h0, hg, st.cuda_stream)
     if rc != 0:
         raise RuntimeError(f"asp_synth_query failed: cuda error {rc}")
+
+
+# Qwen3-8B per-layer parameters (Table 1, head_dim 128): q/o 4096x4096,
+# k/v 4096x1024, MLP 3 x 4096x12288 -> 192.9 M params, 386 MB bf16.
+QWEN3_8B_LAYER_PARAMS = 2 * 4096 * 4096 + 2 * 4096 * 1024 + 3 * 4096 * 12288
+
+
+def synthetic_forward(weights, sink, stream=None) -> None:
+    """The synthetic forward of config [4]: one streaming read of `weights`
+    (a uint8/bf16 device tensor) on `stream`."""
+    import torch
+    st = stream if stream is not None else torch.cuda.current_stream()
+    n_sm = torch.cuda.get_device_properties(weights.device).multi_processor_count
+    nbytes = weights.numel() * weights.element_size()
+    rc = _dev_lib().asp_synth_forward(weights.data_ptr(), nbytes - nbytes % 16, sink.data_ptr(),
+                                      n_sm, st.cuda_stream)
+    if rc != 0:
+        raise RuntimeError(f"asp_synth_forward failed: cuda error {rc}")

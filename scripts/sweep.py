@@ -1,0 +1,125 @@
+"""Sweeps of BASELINE.json configs [3] and [4] on one B200.
+
+    python scripts/sweep.py long-cot          # [3] batch 8, ctx 4k..512k, per-GPU shard of P = 8
+    python scripts/sweep.py high-concurrency  # [4] Qwen3-8B shape, ctx 4k, batch 1..512, a5 overlap
+
+One JSON line per point.  Times are CUDA events on the launching stream over
+`--steps` back-to-back steps after `--warmup`, per step in µs.  Core bytes as
+in bench.py (full-K read + selected K and V).  For [4] the a5 overlap is
+measured with the synthetic forward (a 386 MB weight-streaming read, Qwen3-8B
+layer parameters) on the main stream:
+  t_fwd        forward alone
+  t_sel        a1 predict + a2/a3 score_select alone
+  t_dec        a4 sparse decode alone
+  t_serial     push + select + decode + forward on one stream
+  t_overlapped the AsyncPipeline step (selection for t+1 on a side stream)
+  overlap_eff  (t_serial - t_overlapped) / min(t_fwd, t_sel)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2510_07486_b200 as asp  # noqa: E402
+from paper_2510_07486_b200 import configs, synth  # noqa: E402
+from paper_2510_07486_b200.pipeline import AsyncPipeline  # noqa: E402
+from paper_2510_07486_b200.step import DecodeStep  # noqa: E402
+
+
+def _peak():
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+        return float(json.load(f)["hbm_gbs"])
+
+
+def timed(fn, steps, warmup):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps * 1e3                   # µs per step
+
+
+def point(cfg, args, kv_heads=None, overlap=False):
+    step = DecodeStep(cfg, "cuda", kv_heads=kv_heads, n_fresh=1 if overlap else 0)
+    step.fill_synthetic()
+    torch.cuda.synchronize()
+    hn = step.n_kv
+    core = cfg.core_bytes(hn)
+    t_step = timed(step.run, args.steps, args.warmup)
+    res = {"workload": cfg.name, "batch": cfg.batch, "seq_len": cfg.seq_len, "top_k": cfg.top_k,
+           "kv_heads_on_gpu": hn, "us_per_step": t_step,
+           "hbm_tb_per_s": core / (t_step * 1e-6) / 1e12,
+           "roofline_frac": core / (t_step * 1e-6) / 1e9 / _peak(), "core_bytes": core}
+    if overlap:
+        pipe = AsyncPipeline(step, forward_bytes=2 * synth.QWEN3_8B_LAYER_PARAMS)
+        main = torch.cuda.current_stream()
+        B, D = cfg.batch, cfg.head_dim
+        q_t = torch.randn(B, step.n_q, D, device="cuda")
+        kv_t = torch.randn(2, B, hn, D, device="cuda").to(torch.bfloat16)
+        res["t_fwd"] = timed(lambda: pipe.forward(main), args.steps, args.warmup)
+        res["t_sel"] = timed(lambda: pipe.select(0, main), args.steps, args.warmup)
+        res["t_dec"] = timed(lambda: pipe.decode(0, main), args.steps, args.warmup)
+        res["t_serial"] = timed(lambda: pipe.run_step_serial(q_t, kv_t), args.steps, args.warmup)
+
+        def overlapped():
+            pipe.run_step(q_t, kv_t)
+
+        for _ in range(args.warmup):
+            overlapped()
+        pipe.drain()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            overlapped()
+        pipe.drain()
+        e1.record()
+        torch.cuda.synchronize()
+        res["t_overlapped"] = e0.elapsed_time(e1) / args.steps * 1e3
+        res["overlap_eff"] = ((res["t_serial"] - res["t_overlapped"]) /
+                              min(res["t_fwd"], res["t_sel"]))
+        res["forward_bytes"] = 2 * synth.QWEN3_8B_LAYER_PARAMS
+    del step
+    torch.cuda.empty_cache()
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("sweep", choices=["long-cot", "high-concurrency"])
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    asp.lib()
+    lines = []
+    if args.sweep == "long-cot":
+        for e in range(12, 20):                                # 4k .. 512k
+            cfg = configs.long_cot(1 << e)
+            lines.append(point(cfg, args, kv_heads=(0, 1)))     # per-GPU shard at P = 8
+            print(json.dumps(lines[-1]), flush=True)
+    else:
+        for e in range(0, 10):                                 # batch 1 .. 512
+            cfg = configs.high_concurrency(1 << e)
+            lines.append(point(cfg, args, overlap=True))
+            print(json.dumps(lines[-1]), flush=True)
+    if args.out:
+        with open(args.out, "w") as f:
+            for ln in lines:
+                f.write(json.dumps(ln) + "\n")
+
+
+if __name__ == "__main__":
+    main()

@@ -342,3 +342,71 @@ def test_decode_independent_of_cache_state():
                           out=step.out, workspace=step.ws_dec, params=step.p_dec)
         torch.cuda.synchronize()
         assert torch.equal(step.out, ref)
+
+
+# ----------------------------------------------------------------------------- configs [3], [4]
+def test_long_cot_512k_shard_sampled_rows():
+    """Config [3] at its longest context (512k tokens, k = 32,768) on the
+    per-GPU shard of the 8-GPU run (one KV head): L2-streaming select path,
+    32k-entry decode sets; sampled rows vs the oracle."""
+    cfg = configs.long_cot(524288)
+    step = DecodeStep(cfg, DEV, kv_heads=(5, 1))
+    step.fill_synthetic()
+    step.run()
+    torch.cuda.synchronize()
+    assert int(step.dev_flags.item()) == 0
+    _oracle_row_checks(step, [0, 7])
+    del step
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("batch", [1, 512])
+def test_high_concurrency_sampled_rows(batch):
+    """Config [4] end points: Qwen3-8B shape, 4k context, k = 256."""
+    cfg = configs.high_concurrency(batch)
+    step = DecodeStep(cfg, DEV)
+    step.fill_synthetic()
+    step.run()
+    torch.cuda.synchronize()
+    assert int(step.dev_flags.item()) == 0
+    _oracle_row_checks(step, rows_sample(batch * cfg.n_kv_heads, min(6, batch * 8), seed=4))
+    del step
+    torch.cuda.empty_cache()
+
+
+# ----------------------------------------------------------------------------- a5 async
+def test_async_pipeline_matches_serial():
+    """a5: selection for step t+1 on the side stream, overlapped with step
+    t's decode and the synthetic forward, gives bit-identical idx and out to
+    the same steps run serially on one stream."""
+    from paper_2510_07486_b200.pipeline import AsyncPipeline
+    cfg = configs.high_concurrency(16).with_(seq_len=8192, top_k=512)
+    T = 5
+    g = torch.Generator().manual_seed(11)
+    B, Hq, Hkv, D = cfg.batch, cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim
+    qts = [torch.randn(B, Hq, D, generator=g).to(DEV) for _ in range(T)]
+    qs = [torch.randn(B, Hq, D, generator=g).to(torch.bfloat16).to(DEV) for _ in range(T)]
+    kvs = [torch.randn(2, B, Hkv, D, generator=g).to(torch.bfloat16).to(DEV) for _ in range(T)]
+    runs = []
+    for mode in ("serial", "async"):
+        step = DecodeStep(cfg, DEV, n_fresh=1)
+        step.fill_synthetic()
+        pipe = AsyncPipeline(step, forward_bytes=64 << 20)
+        outs, idxs = [], []
+        for t in range(T):
+            step.q.copy_(qs[t])
+            if mode == "async":
+                pipe.run_step(qts[t], kvs[t])
+            else:
+                pipe.run_step_serial(qts[t], kvs[t])
+            outs.append(step.out.clone())
+            idxs.append(pipe.idx[t % 2].clone())
+        pipe.drain()
+        torch.cuda.synchronize()
+        runs.append((outs, idxs, step))
+    (o_s, i_s, _), (o_a, i_a, _) = runs
+    for t in range(T):
+        assert torch.equal(i_s[t], i_a[t]), t
+        assert torch.equal(o_s[t], o_a[t]), t
+    # the selections really changed as the window and cache moved
+    assert not torch.equal(i_a[0], i_a[T - 1])

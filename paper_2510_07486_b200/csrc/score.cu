@@ -303,6 +303,9 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
         bool nonfinite = false;
         long long pe_full = 0;
         long k = 0;                                 // index of the tile in this CTA's sequence
+        // the scores are read back by the select kernel right after: keep them
+        // L2-resident against the evict-first key stream
+        const uint64_t keep = l2_policy_evict_last();
         for (long i = it.next(it.start); i < it.end; i = it.next(i + 1), k++) {
             if ((k & 1) != group) continue;
             const int a = (int)(k % kAcc);
@@ -339,7 +342,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
             const int tok = j * kTileM + quad * 32 + lane;
             const int len = it.len_of(row);
             if (tok < len) {
-                scores[(size_t)row * p.max_seq_len + tok] = s;
+                st_global_hint(scores + (size_t)row * p.max_seq_len + tok, s, keep);
                 nonfinite |= !isfinite(s);
             }
         }

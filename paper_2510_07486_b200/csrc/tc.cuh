@@ -38,6 +38,16 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
 
 // ---------------------------------------------------------------- TMA
 constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;   // L2 cache hint: streamed once
+
+// An L2 policy that keeps lines resident ahead of evict-first/normal traffic.
+ASP_DEV uint64_t l2_policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+ASP_DEV void st_global_hint(float *ptr, float v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(ptr), "f"(v), "l"(pol) : "memory");
+}
 constexpr uint64_t kEvictNormal = 0x1000000000000000ull;
 
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *map, uint32_t bar,

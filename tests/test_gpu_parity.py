@@ -173,6 +173,33 @@ def test_score_select_long_row_global_path():
     check_selection(idx[0, 0], so[0, 0], L - 11, k)
 
 
+@pytest.mark.parametrize("B,L,k", [(1, 131072, 8192), (3, 65536, 4096), (2, 40962, 2560),
+                                   (1, 9001, 700), (5, 8192, 512)])
+def test_score_select_cluster_split_rows(B, L, k):
+    """Rows split over thread-block clusters (C = 2..16 CTAs, chosen from the
+    row length and the row count) and the small-CTA path: exact sets; ragged
+    lengths put the row end inside a cluster segment."""
+    lens = [L - 37 * b for b in range(B)]
+    idx, _, so, _ = _score_select_case(B, 8, 1, 128, L, k, lens, 60 + B)
+    for b in range(B):
+        check_selection(idx[b, 0], so[b, 0], lens[b], k)
+
+
+def test_score_select_uncached_longest_rows():
+    """Rows beyond 16 x 40,960 tokens: the cluster streams keys from L2."""
+    L, k = 720896, 45056
+    idx, _, so, _ = _score_select_case(1, 8, 1, 128, L, k, [L - 5], 77)
+    check_selection(idx[0, 0], so[0, 0], L - 5, k)
+
+
+def test_score_select_all_equal_keys_long_row():
+    """Massive exact ties on a cluster-split row: the candidate list overflows
+    and the exact fallback must still give the lowest indices."""
+    K = np.zeros((1, 1, 65536, 64), np.uint16)
+    idx, _, _, _ = _score_select_case(1, 8, 1, 64, 65536, 3000, [65536], 3, kv=K)
+    np.testing.assert_array_equal(idx[0, 0], np.arange(3000))
+
+
 # ----------------------------------------------------------------------------- a4 decode
 def _decode_case(B, Hq, Hkv, D, L, idx, seq_lens, n_fresh, seed):
     K = synth.kv_cache(seed, synth.STREAM_K, B, Hkv, L, D)

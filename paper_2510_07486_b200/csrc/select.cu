@@ -65,18 +65,18 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kBins = 4096;
 constexpr int kCand = 2048;                   // candidate slots per CTA
-constexpr int kWarpCand = kCand / kWarps;
 constexpr int kRound = 32768;                 // keys per emission round (bitmap size)
 constexpr int kSampleChunks = 32;             // 32 x 128 consecutive keys sampled per row
 constexpr int kMaxCluster = 16;
+constexpr int kUnroll = 8;                    // 16-B loads in flight per lane (classify)
 
 struct SelectSmem {
     uint32_t hist[kBins];
-    uint32_t cand[kCand];          // candidate keys; warp w: cand[w * kWarpCand ...]
+    uint32_t cand[kCand];          // candidate keys (any order)
     uint32_t cand_idx[kCand];      // their segment offsets
     uint32_t bm_gt[kRound / 32];
     uint32_t bm_eq[kRound / 32];
-    uint32_t n_cand[kWarps];
+    uint32_t n_cand;
     uint32_t warp_a[kWarps], warp_b[kWarps];
     uint32_t scan_total;
     uint32_t found_bin, found_rem, found_bin2;
@@ -150,33 +150,59 @@ __device__ uint32_t block_excl_scan(SelectSmem &s, uint32_t v, uint32_t *total) 
 // Bins holding the rank_a-th and rank_b-th largest elements (1-based,
 // counted from the top bin; rank_a <= rank_b) -> s.found_bin with the rank
 // inside it (s.found_rem), and s.found_bin2.  A rank beyond the total gives
-// bin 0.
-__device__ void find_bucket(SelectSmem &s, int nbins, uint32_t rank_a, uint32_t rank_b) {
-    const int per = nbins / kThreads > 0 ? nbins / kThreads : 1;
+// bin 0.  Thread t owns bins [nbins - PER (t+1), nbins - PER t), read as
+// 16-B vectors; one block scan orders the threads from the top.
+template <int PER>
+__device__ void find_bucket_t(SelectSmem &s, uint32_t rank_a, uint32_t rank_b) {
     const int t = threadIdx.x;
-    const bool owns = t * per < nbins;
+    const int lo = PER * (kThreads - 1 - t);
     if (t == 0) {
         s.found_bin = s.found_bin2 = 0;
         s.found_rem = rank_a;
     }
+    uint32_t c[PER];
+    if constexpr (PER % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < PER; i += 4) {
+            const uint4 v = *reinterpret_cast<const uint4 *>(&s.hist[lo + i]);
+            c[i] = v.x;
+            c[i + 1] = v.y;
+            c[i + 2] = v.z;
+            c[i + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < PER; i++) c[i] = s.hist[lo + i];
+    }
     uint32_t local = 0;
-    if (owns)
-        for (int i = 0; i < per; i++) local += s.hist[nbins - 1 - (t * per + i)];
+#pragma unroll
+    for (int i = 0; i < PER; i++) local += c[i];
     uint32_t total;
     uint32_t above = block_excl_scan(s, local, &total);   // syncs: the init is visible first
-    if (owns) {
-        for (int i = 0; i < per; i++) {
-            const int bin = nbins - 1 - (t * per + i);
-            const uint32_t c = s.hist[bin];
-            if (above < rank_a && above + c >= rank_a) {
-                s.found_bin = (uint32_t)bin;
+    if (above < rank_b && above + local >= rank_a) {
+#pragma unroll
+        for (int i = PER - 1; i >= 0; i--) {
+            const uint32_t cc = c[i];
+            if (above < rank_a && above + cc >= rank_a) {
+                s.found_bin = (uint32_t)(lo + i);
                 s.found_rem = rank_a - above;
             }
-            if (above < rank_b && above + c >= rank_b) s.found_bin2 = (uint32_t)bin;
-            above += c;
+            if (above < rank_b && above + cc >= rank_b) s.found_bin2 = (uint32_t)(lo + i);
+            above += cc;
         }
     }
     __syncthreads();
+}
+
+__device__ __forceinline__ void find_bucket(SelectSmem &s, int nbins, uint32_t rank_a,
+                                            uint32_t rank_b) {
+    if (nbins == kBins) find_bucket_t<kBins / kThreads>(s, rank_a, rank_b);
+    else find_bucket_t<256 / kThreads>(s, rank_a, rank_b);
+}
+
+__device__ __forceinline__ void zero_hist(SelectSmem &s, int nbins) {
+    for (int i = 4 * threadIdx.x; i < nbins; i += 4 * kThreads)
+        *reinterpret_cast<uint4 *>(&s.hist[i]) = make_uint4(0u, 0u, 0u, 0u);
 }
 
 // Sum the first nbins bins of every cluster rank's histogram (rank order)
@@ -232,7 +258,7 @@ __device__ void cluster_counts(SelectSmem &s, int C, int n, uint32_t *tot, uint3
     }
 }
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
 select_kernel(asp_select_params p, const float *__restrict__ scores,
               const int32_t *__restrict__ seq_lens, int32_t *__restrict__ sel_idx,
               uint32_t *dev_flags, int C, int seg_len) {
@@ -283,9 +309,9 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
     };
     const bool direct = n <= kRound;         // the classify sweep can seed the bitmaps
 
-    for (int i = t; i < kBins; i += kThreads) s.hist[i] = 0;
+    zero_hist(s, kBins);
     for (int i = t; i < kRound / 32; i += kThreads) s.bm_eq[i] = 0;
-    if (t < kWarps) s.n_cand[t] = 0;
+    if (t == 0) s.n_cand = 0;
     __syncthreads();
 #ifdef ASP_PROFILE_SELECT
     long long _tp = clock64();
@@ -304,7 +330,7 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
 #pragma unroll
         for (int u = 0; u < kPerWarp; u++) {
             const int j = warp + u * kWarps;
-            so[u] = j < ns ? ((int)((long)j * row_chunks / ns) << 7) + 4 * lane : len;
+            so[u] = j < ns ? ((j * row_chunks / ns) << 7) + 4 * lane : len;   // < 2^31
             sv[u] = raw4(row, so[u], len);
         }
 #pragma unroll
@@ -315,8 +341,10 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
 #pragma unroll
         for (int c = 0; c < 4; c++)
             if (so[u] + c < len) atomicAdd(&s.hist[comp(sk[u], c) >> 20], 1u);
-    uint32_t m = 0;                                       // sample size
-    for (int j = 0; j < ns; j++) m += min(128, len - (int)(((long)j * row_chunks / ns) << 7));
+    // sample size: ns full chunks, unless the last one sampled is the row's
+    // partial last chunk
+    uint32_t m = 128u * ns;
+    if ((ns - 1) * row_chunks / ns == row_chunks - 1) m -= (uint32_t)(row_chunks * 128 - len);
     __syncthreads();
     SPROF(0);
     // bracket T between sample ranks r -/+ delta (1-based from the top)
@@ -332,7 +360,7 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
     uint32_t key_lo = bin_lo << 20, key_hi = ((bin_hi + 1) << 20) - 1u;
     if (bin_hi - bin_lo < 16) {
         // second level: 8 more bits (19:12) over the bracketed samples
-        for (int i = t; i < kBins; i += kThreads) s.hist[i] = 0;
+        zero_hist(s, kBins);
         __syncthreads();
 #pragma unroll
         for (int u = 0; u < kPerWarp; u++)
@@ -351,33 +379,39 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
     }
     SPROF(1);
 
-    // ---- 2. classify the segment: count keys above the bracket (and, for a
-    // direct emission, mark them in bm_gt), compact the bracketed ones
-    // (key, offset) into per-warp lists; NaN detection rides along.  A warp
-    // step covers 128 consecutive keys, 4 per lane (one 16-B load).  The
-    // bracket is compared in fp32 -- v >= lb(K) <=> key(v) >= K -- so a
-    // key is only formed for the few candidates.
+    // ---- 2. classify the segment: count the keys above the bracket and
+    // collect the bracketed ones (key, offset) into the candidate list; NaN
+    // detection rides along.  A warp step covers 128 consecutive keys, 4 per
+    // lane (one 16-B load).  The bracket is compared in fp32 -- v >= lb(K)
+    // <=> key(v) >= K -- so a key is only formed for the few candidates.
+    // Direct segments (<= kRound keys) only mark both classes in bitmaps
+    // (bm_gt: above, bm_eq: candidate) and gather the candidates afterwards.
     const int nchunks = (n + 127) >> 7;
     const float f_lo = key_lower_bound(key_lo);
     const float f_above = key_lower_bound((uint64_t)key_hi + 1);
     bool nan = false;
     {
-        uint32_t *wc = s.cand + warp * kWarpCand;
-        uint32_t *wi = s.cand_idx + warp * kWarpCand;
         uint32_t above = 0;
-        for (int c0 = warp; c0 < nchunks; c0 += 4 * kWarps) {
-            float4 kv[4];
+        for (int c0 = warp; c0 < nchunks; c0 += kUnroll * kWarps) {
+            const bool full = vec && ((c0 + (kUnroll - 1) * kWarps) << 7) + 128 <= n;
+            float4 kv[kUnroll];
+            if (full) {
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const int ch = c0 + u * kWarps;
-                kv[u] = raw4(srow, (ch << 7) + 4 * lane, ch < nchunks ? n : 0);
+                for (int u = 0; u < kUnroll; u++)
+                    kv[u] = __ldg(reinterpret_cast<const float4 *>(srow + ((c0 + u * kWarps) << 7)) + lane);
+            } else {
+#pragma unroll
+                for (int u = 0; u < kUnroll; u++) {
+                    const int ch = c0 + u * kWarps;
+                    kv[u] = raw4(srow, (ch << 7) + 4 * lane, ch < nchunks ? n : 0);
+                }
             }
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < kUnroll; u++) {
                 const int ch = c0 + u * kWarps;
                 if (ch >= nchunks) break;                      // warp-uniform
                 const int o = (ch << 7) + 4 * lane;
-                const uint32_t valid = o + 3 < n ? 0xFu : (0xFu >> min(4, o + 4 - n)) & 0xFu;
+                const uint32_t valid = full || o + 3 < n ? 0xFu : (0xFu >> min(4, o + 4 - n)) & 0xFu;
                 uint32_t ab = 0, in = 0;
 #pragma unroll
                 for (int c = 0; c < 4; c++) {
@@ -390,19 +424,24 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
                 in &= valid & ~ab;
                 above += __popc(ab);
                 if (direct) {                 // word ch*4 + lane/8 <- nibbles of 8 lanes
-                    uint32_t wgt = ab << (4 * (lane & 7));
+                    uint32_t wa = ab << (4 * (lane & 7)), wc = in << (4 * (lane & 7));
 #pragma unroll
-                    for (int d = 1; d < 8; d <<= 1) wgt |= __shfl_xor_sync(0xffffffffu, wgt, d);
-                    if ((lane & 7) == 0) s.bm_gt[(ch << 2) + (lane >> 3)] = wgt;
-                }
-                if (in) {                     // order within the list is irrelevant
-                    uint32_t slot = atomicAdd(&s.n_cand[warp], (uint32_t)__popc(in));
+                    for (int d = 1; d < 8; d <<= 1) {
+                        wa |= __shfl_xor_sync(0xffffffffu, wa, d);
+                        wc |= __shfl_xor_sync(0xffffffffu, wc, d);
+                    }
+                    if ((lane & 7) == 0) {
+                        s.bm_gt[(ch << 2) + (lane >> 3)] = wa;
+                        s.bm_eq[(ch << 2) + (lane >> 3)] = wc;
+                    }
+                } else if (in) {              // order within the list is irrelevant
+                    uint32_t slot = atomicAdd(&s.n_cand, (uint32_t)__popc(in));
 #pragma unroll
                     for (int c = 0; c < 4; c++) {
                         if ((in >> c) & 1u) {
-                            if (slot < (uint32_t)kWarpCand) {
-                                wc[slot] = asp::score_key(comp(kv[u], c));
-                                wi[slot] = (uint32_t)(o + c);
+                            if (slot < (uint32_t)kCand) {
+                                s.cand[slot] = asp::score_key(comp(kv[u], c));
+                                s.cand_idx[slot] = (uint32_t)(o + c);
                             }
                             slot++;
                         }
@@ -410,16 +449,30 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
                 }
             }
         }
-        __syncwarp();
-        const uint32_t nc = s.n_cand[warp];
         above = warp_sum_u32(above);
         const uint32_t a = block_sum_warps(s, above);
-        const uint32_t c = block_sum_warps(s, nc);
-        const uint32_t over = block_sum_warps(s, nc > (uint32_t)kWarpCand ? 1u : 0u);
+        if (direct) {                         // gather the marked candidates; clear bm_eq
+            for (int w = t; w < ((nchunks << 2)); w += kThreads) {
+                uint32_t bits = s.bm_eq[w];
+                if (!bits) continue;
+                s.bm_eq[w] = 0;
+                uint32_t slot = atomicAdd(&s.n_cand, (uint32_t)__popc(bits));
+                while (bits) {
+                    const int o = (w << 5) + __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    if (slot < (uint32_t)kCand) {
+                        s.cand[slot] = key_at(o);
+                        s.cand_idx[slot] = (uint32_t)o;
+                    }
+                    slot++;
+                }
+            }
+        }
+        __syncthreads();
         if (t == 0) {
             s.cnt[0] = a;
-            s.cnt[1] = c;
-            s.cnt[2] = over;
+            s.cnt[1] = s.n_cand;
+            s.cnt[2] = s.n_cand > (uint32_t)kCand ? 1u : 0u;
         }
     }
     uint32_t tot[3], bef[3];
@@ -437,21 +490,19 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
     // fn(key, candidate slot or -1)
     auto for_each_key = [&](auto &&fn) {
         if (use_cand) {
-            for (int e = t; e < kCand; e += kThreads) {
-                const int w = e / kWarpCand, j = e - w * kWarpCand;
-                if ((uint32_t)j < s.n_cand[w]) fn(s.cand[e], e);
-            }
+            const int nc = (int)s.n_cand;
+            for (int e = t; e < nc; e += kThreads) fn(s.cand[e], e);
         } else {
             for (int o = t; o < n; o += kThreads) fn(key_at(o), -1);
         }
     };
-    for (int i = t; i < kBins; i += kThreads) s.hist[i] = 0;
+    zero_hist(s, kBins);
     __syncthreads();
     for_each_key([&](uint32_t key, int) { atomicAdd(&s.hist[key >> 20], 1u); });
     merge_hist(s, kBins, C);
     find_bucket(s, kBins, rank0, rank0);
     const uint32_t d1 = s.found_bin, rem1 = s.found_rem;
-    for (int i = t; i < kBins; i += kThreads) s.hist[i] = 0;
+    zero_hist(s, kBins);
     __syncthreads();
     for_each_key([&](uint32_t key, int) {
         if ((key >> 20) == d1) atomicAdd(&s.hist[(key >> 8) & 0xFFFu], 1u);
@@ -459,7 +510,7 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
     merge_hist(s, kBins, C);
     find_bucket(s, kBins, rem1, rem1);
     const uint32_t pre24 = (d1 << 12) | s.found_bin, rem2 = s.found_rem;
-    for (int i = t; i < 256; i += kThreads) s.hist[i] = 0;
+    zero_hist(s, 256);
     __syncthreads();
     for_each_key([&](uint32_t key, int) {
         if ((key >> 8) == pre24) atomicAdd(&s.hist[key & 0xFFu], 1u);

@@ -39,7 +39,7 @@ __device__ unsigned long long g_dec_prof[16];
     do {                                                                                 \
         const long long _t0 = clock64();                                                 \
         call;                                                                            \
-        if (threadIdx.x == 0 || threadIdx.x == kMmaWarp * 32 || threadIdx.x == 128)       \
+        if (threadIdx.x == 0 || threadIdx.x == kMmaWarp * 32 || threadIdx.x == kProducerThreads) \
             atomicAdd(&g_dec_prof[idx], (unsigned long long)(clock64() - _t0));          \
     } while (0)
 #else
@@ -54,10 +54,10 @@ constexpr int kTile = 128;                  // tokens per tile
 constexpr int kChunk = 256;                 // entries per work item (fixed: determinism)
 constexpr int kTilesPerItem = kChunk / kTile;
 constexpr int kN = 16;                      // MMA N: G heads (MMA1) / 2G hi-lo rows (MMA2)
-constexpr int kProducerWarps = 4;
+constexpr int kProducerWarps = 8;
 constexpr int kProducerThreads = kProducerWarps * 32;
-constexpr int kMmaWarp = 8;
-constexpr int kThreads = 9 * 32;             // 4 producer, 4 softmax/epilogue, 1 MMA warp
+constexpr int kMmaWarp = kProducerWarps + 4;
+constexpr int kThreads = (kProducerWarps + 5) * 32;   // producers, 4 softmax/epilogue, 1 MMA warp
 constexpr float kLog2e = 1.4426950408889634f;
 
 template <int D>
@@ -172,7 +172,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
         // software pipeline: the selection indices and row length of the NEXT item
         // are loaded while the current one is being gathered
         constexpr int kEntriesPerThread = kChunk / kProducerThreads;
-        int pre_raw[kEntriesPerThread] = {0, 0};
+        int pre_raw[kEntriesPerThread] = {};
         int pre_len = 0;
         auto fetch = [&](int i) {
             const Item it = item(i);
@@ -189,7 +189,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
         int pending[kLag + 1];
         int npend = 0;
         auto release_oldest = [&]() {
-            asm volatile("cp.async.wait_group %0;" ::"n"(kLag) : "memory");
+            DWAIT(11, asm volatile("cp.async.wait_group %0;" ::"n"(kLag) : "memory"));
             fence_proxy_async_smem();
             mbar_arrive(bar(B_FULL + pending[0]));
             for (int u = 1; u < npend; u++) pending[u - 1] = pending[u];
@@ -219,7 +219,9 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             }
             // this item's indices were fetched one item ahead (pre_*); fetch the next
             const int len = min(max(pre_len, 0), p.max_seq_len);
-            const int raw[kEntriesPerThread] = {pre_raw[0], pre_raw[1]};
+            int raw[kEntriesPerThread];
+#pragma unroll
+            for (int u = 0; u < kEntriesPerThread; u++) raw[u] = pre_raw[u];
             if (i + 1 < n_items) fetch(i + 1);
             DWAIT(1, mbar_wait(bar(B_TOKEMPTY + slot), ((i >> 1) & 1) ^ 1));
             // WAR: every producer thread must be done reading this slot for the
@@ -255,17 +257,25 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             constexpr int kRowsPerPass = kProducerThreads / kChunksPerRow;
             const int chunk = pt % kChunksPerRow;
             const int region = chunk / 8, cc = chunk % 8;
+            constexpr int kPerThread = kTile / kRowsPerPass;  // rows r0 + kRowsPerPass * u
+            const int r0 = pt / kChunksPerRow;
+            const asp_bf16 *src0 = rowbase + chunk * 8;
             for (int t = 0; t < kTilesPerItem; t++) {
                 DWAIT(2, mbar_wait(bar(B_EMPTY + s), ph ^ 1));
-                const uint32_t stage = stage0 + s * C::kStageBytes + region * (kTile * 128);
-                const int32_t *tk = s_tok + slot * kChunk + t * kTile;
-#pragma unroll 4
-                for (int r = pt / kChunksPerRow; r < kTile; r += kRowsPerPass) {
-                    const int tok = max(tk[r], 0);            // invalid entries read token 0
-                    const asp_bf16 *src = rowbase + (int64_t)tok * st + chunk * 8;
-                    const uint32_t dst = stage + r * 128 + ((cc ^ (r & 7)) * 16);
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src)
-                                 : "memory");
+                // rows r0 + 8u share (r & 7): one swizzle per thread
+                const uint32_t dst0 = stage0 + s * C::kStageBytes + region * (kTile * 128) +
+                                      r0 * 128 + ((cc ^ (r0 & 7)) * 16);
+                const int32_t *tk = s_tok + slot * kChunk + t * kTile + r0;
+                // all token loads first, then the copies back to back (no memory
+                // clobber on the copies: they are ordered by commit / wait_group)
+                int tok[kPerThread];
+#pragma unroll
+                for (int u = 0; u < kPerThread; u++) tok[u] = max(tk[u * kRowsPerPass], 0);  // -1 -> row 0
+#pragma unroll
+                for (int u = 0; u < kPerThread; u++) {
+                    const asp_bf16 *src = src0 + (int64_t)tok[u] * st;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                                 ::"r"(dst0 + (uint32_t)(u * kRowsPerPass * 128)), "l"(src));
                 }
                 // cp.async writes are generic-proxy: each producer waits for its group
                 // from kLag tiles ago, fences it to the async proxy (tensor core), and

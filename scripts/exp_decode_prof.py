@@ -21,6 +21,6 @@ for it in range(3):
 L.asp_decode_prof_read(buf)
 print("decode call us", ev[0].elapsed_time(ev[1]) * 1000)
 names = ["P qempty", "P tokempty", "P stage-empty", "M stage-full", "M qfull", "M pfull", "M oempty",
-         "S tokfull", "S sfull", "E ofull", "cta total"]
+         "S tokfull", "S sfull", "E ofull", "cta total", "P cp.async wait"]
 for n, v in zip(names, buf):
     print(f"{n:14s} {v / 148 / 1.93e3:8.1f} us/CTA")

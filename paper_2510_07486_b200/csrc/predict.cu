@@ -7,41 +7,63 @@
 // R1-R8 of DESIGN.md §3 (masked-shared default).  All regression arithmetic
 // is fp64 (reading R16).
 //
-// Design (B200): one warp per (batch, q-head) row, four independent rows per
-// CTA, no CTA-wide barriers.
-//   * The W x D window is staged once in shared memory (fp32, logical ring
-//     order, row stride D+4 so the tensor-core fragment loads are
-//     bank-conflict free) with 8 x 16-B loads in flight per lane.
+// Design (B200): one warp per (batch, q-head) row, eight independent rows
+// per CTA, no CTA-wide barriers.  The per-row work is a chain of small
+// dependent steps, so the kernel is built for occupancy: ~5 KB of shared
+// memory and <= 64 registers per warp put 32 rows on every SM at once (the
+// 4096 rows of config [2] in one wave) so the chains overlap.
 //   * The augmented Gram matrix G' = Q Q^T (W x W) -- the history Gram G0
 //     AND beta = H y in its last row -- runs on the fp64 tensor cores
-//     (mma.sync m8n8k4 f64), all 8x8 tiles interleaved per k-step.
+//     (mma.sync m8n8k4 f64), all 8x8 tiles interleaved per k-step; the
+//     fragments are read straight from the window in global memory in
+//     logical ring order (each element once; lines reused through L1).
+//   * For W <= 17 the ridge system lives in registers (lane i: row i of
+//     [G0 + eps I | beta]) and is solved by Gauss-Jordan elimination with
+//     shuffled pivot rows; longer windows use a shared-memory Cholesky.
 //   * Cholesky of G0 + eps I is lane-parallel over the rows below each pivot;
 //     forward / backward substitution keep the right-hand side in registers
 //     (lane j owns component j) and broadcast pivots by shuffle.
 //   * The masked-shared weights collapse to W coefficients c_p (one exp per
 //     history weight, prefix sums by shuffle; a row-prefix softmax is the
 //     prefix's normalised exponentials), so q_hat = sum_p c_p Q[p] / m is one
-//     pass over the staged window, rounded once to fp32.
+//     coalesced pass over the (cache-hot) window, rounded once to fp32.
 // The step is ~0.7% of the path's bytes ("negligible runtime").
 #include "common.cuh"
 
 #include <math.h>
 
+#ifdef ASP_PROFILE_PREDICT
+__device__ unsigned long long g_pred_prof[8];
+#define PPROF(idx)                                                                       \
+    do {                                                                                 \
+        if ((threadIdx.x & 31) == 0) {                                                   \
+            const long long _t = clock64();                                              \
+            atomicAdd(&g_pred_prof[idx], (unsigned long long)(_t - _tp));                \
+            _tp = _t;                                                                    \
+        }                                                                                \
+    } while (0)
+extern "C" __attribute__((visibility("default"))) int asp_predict_prof_read(unsigned long long *h) {
+    cudaMemcpyFromSymbol(h, g_pred_prof, sizeof(g_pred_prof));
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_pred_prof, z, sizeof(z));
+    return 0;
+}
+#else
+#define PPROF(idx) (void)0
+#endif
+
 namespace {
 
-constexpr int kWarps = 4;
+constexpr int kWarps = 8;
 
-__host__ __device__ size_t warp_smem_bytes(int W, int D) {
-    const int Wp = (W + 7) & ~7;
-    const size_t b = (size_t)Wp * (D + 4) * sizeof(float)            // staged window
-                     + (size_t)W * W * sizeof(double)                // augmented Gram G'
+__host__ __device__ size_t warp_smem_bytes(int W) {
+    const size_t b = (size_t)W * W * sizeof(double)                  // augmented Gram G'
                      + (size_t)(W > 1 ? (W - 1) * (W - 1) : 1) * sizeof(double)  // Cholesky
                      + (size_t)(64 + 32 + 32) * sizeof(double);      // scratch, exps, coeffs
     return (b + 15) & ~(size_t)15;                                   // next warp: 16-B aligned
 }
 
 struct WarpSmem {
-    float *win;     // [Wp][D+4]
     double *G;      // [W][W] augmented Gram
     double *A;      // [nh][nh] Cholesky working copy
     double *vec;    // [64]
@@ -59,21 +81,36 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-// G' = Q Q^T over the staged window (NB 8-row blocks), fp64 tensor cores.
+// G' = Q Q^T over the window (NB 8-row blocks of logical rows; physical
+// row of logical i = (ring_start + i) % W), fp64 tensor cores.  Every window
+// element is loaded exactly once (by the lane owning its fragment slot), so
+// the finiteness check rides along; returns it (warp-uniform).
 template <int D, int NB>
-__device__ void gram_dmma(const WarpSmem &s, int W) {
+__device__ bool gram_dmma(const WarpSmem &s, const float *__restrict__ win, int W, int ring_start) {
     const int lane = threadIdx.x & 31;
     const int fr = lane >> 2, fc = lane & 3;
     constexpr int kTiles = NB * (NB + 1) / 2;
     double acc[kTiles][2];
 #pragma unroll
     for (int t = 0; t < kTiles; t++) acc[t][0] = acc[t][1] = 0.0;
-    const float *base = s.win + fr * (D + 4) + fc;
+    const float *rp[NB];
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+        const int i = 8 * b + fr;                     // logical row of this lane's fragment
+        int phys = i + ring_start;
+        if (phys >= W) phys -= W;
+        rp[b] = i < W ? win + (size_t)phys * D + fc : nullptr;
+    }
+    bool finite = true;
 #pragma unroll 4
     for (int k = 0; k < D; k += 4) {
         double f[NB];
 #pragma unroll
-        for (int b = 0; b < NB; b++) f[b] = (double)base[b * 8 * (D + 4) + k];
+        for (int b = 0; b < NB; b++) {
+            const float x = rp[b] ? __ldg(rp[b] + k) : 0.0f;
+            finite = finite && isfinite(x);
+            f[b] = (double)x;
+        }
         int t = 0;
 #pragma unroll
         for (int bi = 0; bi < NB; bi++)
@@ -94,6 +131,7 @@ __device__ void gram_dmma(const WarpSmem &s, int W) {
                     s.G[j * W + i] = acc[t][e];
                 }
             }
+    return __all_sync(0xffffffffu, finite);
 }
 
 // Ridge solve over history rows [h0, h0 + nh) regressing the newest row W-1
@@ -165,6 +203,52 @@ __device__ double ridge_solve(const WarpSmem &s, int W, int h0, int nh, float ep
     return lane < nh ? r : 0.0;
 }
 
+// The same ridge solve for the full history (h0 = 0, nh <= 16) with the
+// system in registers: lane i holds row i of [G0 + eps I | beta] and
+// Gauss-Jordan elimination (no pivoting: the matrix is SPD, its pivots are
+// Cholesky's squared diagonal -- a pivot <= 0 means not positive definite)
+// broadcasts one pivot row per step by shuffle.  ~15 dependent steps of
+// independent shuffles and FMAs instead of the shared-memory Cholesky.
+__device__ double ridge_solve_regs(const WarpSmem &s, int W, int nh, float eps, bool absolute,
+                                   bool &ok) {
+    constexpr int kMax = 16;
+    const int lane = threadIdx.x & 31;
+    const bool own = lane < nh;
+    double r[kMax];
+#pragma unroll
+    for (int k = 0; k < kMax; k++) r[k] = (own && k < nh) ? s.G[lane * W + k] : 0.0;
+    double rb = own ? s.G[(W - 1) * W + lane] : 0.0;
+    // eps relative to mean diag(G0) (reading R7) unless absolute; zero floor
+    double e = (double)eps;
+    if (!absolute) {
+        double tr = own ? s.G[lane * W + lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+        e = (double)eps * (tr / nh);
+    }
+    if (e == 0.0) e = 1e-30;
+#pragma unroll
+    for (int k = 0; k < kMax; k++) if (k == lane && own) r[k] += e;
+    ok = true;
+    double diag = 1.0;                                                 // lane j: pivot j
+#pragma unroll
+    for (int j = 0; j < kMax; j++) {
+        if (j >= nh) break;
+        const double d = __shfl_sync(0xffffffffu, r[j], j);
+        const double pb = __shfl_sync(0xffffffffu, rb, j);
+        if (!(d > 0.0) || !isfinite(d)) { ok = false; break; }        // warp-uniform
+        if (lane == j) diag = d;
+        const double f = lane != j ? r[j] / d : 0.0;                   // the pivot row stays
+#pragma unroll
+        for (int k = j; k < kMax; k++) r[k] = fma(-f, __shfl_sync(0xffffffffu, r[k], j), r[k]);
+        rb = fma(-f, pb, rb);
+    }
+    if (!ok) return 0.0;
+    const double x = own ? rb / diag : 0.0;
+    ok = __all_sync(0xffffffffu, !own || isfinite(x));
+    return x;
+}
+
 // Collapse the masked-shared assembly (Alg. 1 Steps 4-6, readings R4-R6) of
 // the weights v[0..n) (lane i holds v_i) into coefficients c[0..W) (smem):
 // row j = 1..W uses r_j = softmax(v[0..n_j)), n_j = min(j, n), on the newest
@@ -222,21 +306,19 @@ __device__ double lane_softmax(double v_lane, int n) {
 }
 
 template <int D, int NB>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, 4)
 predict_kernel(asp_predict_params p, const float *__restrict__ q_window,
                float *__restrict__ q_hat, uint32_t *dev_flags) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int LD = D + 4;
     const int W = p.window, n = W - 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long rows = (long)p.batch * p.n_q_heads;
     const long row = (long)blockIdx.x * kWarps + warp;
     if (row >= rows) return;
 
-    unsigned char *base = smem_raw + warp_smem_bytes(W, D) * warp;
+    unsigned char *base = smem_raw + warp_smem_bytes(W) * warp;
     WarpSmem s;
-    s.win = reinterpret_cast<float *>(base);
-    size_t off = (size_t)NB * 8 * LD * sizeof(float);
+    size_t off = 0;
     s.G = reinterpret_cast<double *>(base + off);
     off += (size_t)W * W * sizeof(double);
     s.A = reinterpret_cast<double *>(base + off);
@@ -244,49 +326,28 @@ predict_kernel(asp_predict_params p, const float *__restrict__ q_window,
     s.vec = reinterpret_cast<double *>(base + off);
     s.e = s.vec + 64;
     s.c = s.e + 32;
-
-    // Step 1: stage the window in logical order (physical slot
-    // ring_start + j holds logical j); zero the padding rows.
-    const float *src = q_window + (size_t)row * W * D;
-    bool finite = true;
-    constexpr int kVecsPerRow = D / 4;
-    const int vecs = W * kVecsPerRow;
-    constexpr int kBatch = 8;
-    for (int v0 = 0; v0 < vecs; v0 += 32 * kBatch) {
-        float4 x[kBatch];
-#pragma unroll
-        for (int u = 0; u < kBatch; u++) {
-            const int v = v0 + u * 32 + lane;
-            x[u] = v < vecs ? __ldg(reinterpret_cast<const float4 *>(src) + v)
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int u = 0; u < kBatch; u++) {
-            const int v = v0 + u * 32 + lane;
-            if (v >= vecs) break;
-            const int phys = v / kVecsPerRow, d = (v % kVecsPerRow) * 4;
-            int logical = phys - p.ring_start;
-            if (logical < 0) logical += W;
-            *reinterpret_cast<float4 *>(s.win + logical * LD + d) = x[u];
-            finite = finite && isfinite(x[u].x) && isfinite(x[u].y) && isfinite(x[u].z) &&
-                     isfinite(x[u].w);
-        }
-    }
-    for (int i = W * LD + lane * 4; i < NB * 8 * LD; i += 128)
-        *reinterpret_cast<float4 *>(s.win + i) = make_float4(0.f, 0.f, 0.f, 0.f);
-    finite = __all_sync(0xffffffffu, finite);
     s.c[lane] = 0.0;
-    __syncwarp();
 
+    // Step 1: the window's logical row i is physical row
+    // (ring_start + i) % W; row W-1 is the newest query.
+    const float *src = q_window + (size_t)row * W * D;
+    auto phys_of = [&](int i) {
+        const int ph = i + p.ring_start;
+        return ph >= W ? ph - W : ph;
+    };
     float *out = q_hat + (size_t)row * D;
     const uint32_t mode = p.flags & 0xFu;
     const double sgn = (p.flags & ASP_SIGN_NEGATED) ? -1.0 : 1.0;
     const bool absolute = (p.flags & ASP_EPS_ABSOLUTE) != 0;
 
+#ifdef ASP_PROFILE_PREDICT
+    long long _tp = clock64();
+#endif
+    const bool finite = W > 1 ? gram_dmma<D, NB>(s, src, W, p.ring_start) : true;
+    PPROF(0);
     bool ok = finite && W > 1;
     double denom = 1.0;
     if (ok) {
-        gram_dmma<D, NB>(s, W);
         __syncwarp();
         if (mode == ASP_ASSEMBLY_PER_WINDOW) {
             // Eq. 5 literal: one solve per window size k = 1..n on Q[W-1-k..W-2],
@@ -304,7 +365,9 @@ predict_kernel(asp_predict_params p, const float *__restrict__ q_window,
             s.c[lane] = cacc;
             denom = (double)n;
         } else {
-            const double om = ridge_solve(s, W, 0, n, p.eps, absolute, ok);
+            const double om = n <= 16 ? ridge_solve_regs(s, W, n, p.eps, absolute, ok)
+                                      : ridge_solve(s, W, 0, n, p.eps, absolute, ok);
+            PPROF(1);
             if (ok && mode == ASP_ASSEMBLY_SINGLE) {
                 // Eq. 4: omega[i] (history row i) weights Q[i+1].
                 const double w = (p.flags & ASP_NORM_NONE) ? om : lane_softmax(sgn * om, n);
@@ -319,16 +382,25 @@ predict_kernel(asp_predict_params p, const float *__restrict__ q_window,
         }
         __syncwarp();
     }
+    PPROF(2);
     if (ok) {
         const double inv_m = 1.0 / denom;
-        for (int d = lane; d < D; d += 32) {
-            double acc = 0.0;
-            for (int q = 0; q < W; q++) acc = fma(s.c[q], (double)s.win[q * LD + d], acc);
-            out[d] = (float)(acc * inv_m);
+        double acc[D / 32];
+#pragma unroll
+        for (int j = 0; j < D / 32; j++) acc[j] = 0.0;
+        for (int q = 0; q < W; q++) {
+            const double cq = s.c[q];
+            const float *rq = src + (size_t)phys_of(q) * D + lane;
+#pragma unroll
+            for (int j = 0; j < D / 32; j++) acc[j] = fma(cq, (double)__ldg(rq + 32 * j), acc[j]);
         }
+#pragma unroll
+        for (int j = 0; j < D / 32; j++) out[lane + 32 * j] = (float)(acc[j] * inv_m);
+        PPROF(3);
     } else {
         // Passthrough q_hat = Q_t; flag why.
-        for (int d = lane; d < D; d += 32) out[d] = s.win[(W - 1) * LD + d];
+        const float *rq = src + (size_t)phys_of(W - 1) * D;
+        for (int d = lane; d < D; d += 32) out[d] = rq[d];
         if (lane == 0 && W > 1) asp::flag_or(dev_flags, finite ? ASP_FLAG_NOT_PD : ASP_FLAG_NONFINITE);
     }
 }
@@ -337,7 +409,7 @@ template <int D, int NB>
 cudaError_t launch(const asp_predict_params &p, const float *q_window, float *q_hat,
                    uint32_t *dev_flags, cudaStream_t s) {
     const long rows = (long)p.batch * p.n_q_heads;
-    const size_t smem = warp_smem_bytes(p.window, D) * kWarps;
+    const size_t smem = warp_smem_bytes(p.window) * kWarps;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(predict_kernel<D, NB>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -38,6 +38,16 @@ ASP_DEV uint32_t score_key(float f) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+// Programmatic dependent launch (PDL): every kernel of the path is launched
+// with programmatic stream serialization, so its prologue (barrier init,
+// TMEM allocation, descriptor prefetch) overlaps the previous kernel's tail.
+// pdl_wait() must precede the first global-memory access of every kernel
+// (it returns once the preceding grid has completed and its writes are
+// visible -- transitively, every earlier kernel in the stream);
+// pdl_trigger() lets the next kernel in the stream start launching.
+ASP_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+ASP_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 ASP_DEV void flag_or(uint32_t *dev_flags, uint32_t bits) {
     if (dev_flags && bits) atomicOr(dev_flags, bits);
 }
@@ -54,6 +64,30 @@ ASP_DEV float2 ffma2(float2 a, float2 b, float2 c) {
 }
 
 }  // namespace asp
+
+// Launch `kern` with programmatic stream serialization (PDL) and an optional
+// thread-block cluster size (1 = none).
+template <typename... KArgs, typename... Args>
+cudaError_t asp_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, unsigned cluster, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = cluster;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = cluster > 1 ? 2 : 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<Args &&>(args)...);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
 
 // Internal launchers (implemented per kernel file, called by abi.cu after
 // host-side validation).  They return cudaGetLastError() of the launch.

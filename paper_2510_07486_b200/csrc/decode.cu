@@ -153,6 +153,8 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder_g;
+    asp::pdl_wait();                        // q, the caches, idx and partials are ours now
+    asp::pdl_trigger();
 #ifdef ASP_PROFILE_DECODE
     const long long t_k0 = clock64();
 #endif
@@ -513,6 +515,8 @@ __global__ void __launch_bounds__(D)
 decode_combine_kernel(asp_decode_params p, const float *__restrict__ partials,
                       float *__restrict__ out, int n_splits) {
     const int hq = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
+    asp::pdl_wait();
+    asp::pdl_trigger();
     const float *src = partials + ((size_t)b * p.n_q_heads + hq) * n_splits * (D + 2);
     float M = -INFINITY;
     for (int s = 0; s < n_splits; s++) M = fmaxf(M, src[(size_t)s * (D + 2)]);
@@ -544,12 +548,11 @@ cudaError_t launch(const asp_decode_params &p, const asp_bf16 *q, const asp_bf16
     cudaError_t e = cudaFuncSetAttribute(decode_tc_kernel<D, G>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
-    decode_tc_kernel<D, G><<<grid, kThreads, C::kSmemBytes, s>>>(p, q, k, v, seq_lens, idx,
-                                                                 partials, ns);
-    e = cudaGetLastError();
+    e = asp_launch(decode_tc_kernel<D, G>, dim3(grid), dim3(kThreads), C::kSmemBytes, s, 1, p, q,
+                   k, v, seq_lens, idx, partials, ns);
     if (e != cudaSuccess) return e;
-    decode_combine_kernel<D><<<dim3(p.n_q_heads, p.batch), D, 0, s>>>(p, partials, out, ns);
-    return cudaGetLastError();
+    return asp_launch(decode_combine_kernel<D>, dim3(p.n_q_heads, p.batch), dim3(D), 0, s, 1, p,
+                      (const float *)partials, out, ns);
 }
 
 }  // namespace

@@ -314,6 +314,8 @@ predict_kernel(asp_predict_params p, const float *__restrict__ q_window,
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long rows = (long)p.batch * p.n_q_heads;
     const long row = (long)blockIdx.x * kWarps + warp;
+    asp::pdl_wait();
+    asp::pdl_trigger();
     if (row >= rows) return;
 
     unsigned char *base = smem_raw + warp_smem_bytes(W) * warp;
@@ -416,8 +418,8 @@ cudaError_t launch(const asp_predict_params &p, const float *q_window, float *q_
         if (e != cudaSuccess) return e;
     }
     const unsigned grid = (unsigned)((rows + kWarps - 1) / kWarps);
-    predict_kernel<D, NB><<<grid, kWarps * 32, smem, s>>>(p, q_window, q_hat, dev_flags);
-    return cudaGetLastError();
+    return asp_launch(predict_kernel<D, NB>, dim3(grid), dim3(kWarps * 32), smem, s, 1, p, q_window,
+                      q_hat, dev_flags);
 }
 
 }  // namespace

@@ -158,6 +158,8 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder_g;
+    asp::pdl_wait();                        // q_hat, seq_lens and the score buffer are ours now
+    asp::pdl_trigger();
 #ifdef ASP_PROFILE_SCORE
     const long long t_kernel0 = clock64();
 #endif
@@ -397,9 +399,8 @@ cudaError_t launch(const asp_select_params &p, const float *q_hat, const asp_bf1
     cudaError_t e = cudaFuncSetAttribute(score_tc_kernel<D, G>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
-    score_tc_kernel<D, G><<<grid, kThreads, C::kSmemBytes, s>>>(map, p, q_hat, seq_lens, scores,
-                                                                dev_flags, tpr);
-    return cudaGetLastError();
+    return asp_launch(score_tc_kernel<D, G>, dim3(grid), dim3(kThreads), C::kSmemBytes, s, 1, map,
+                      p, q_hat, seq_lens, scores, dev_flags, tpr);
 }
 
 }  // namespace

@@ -268,6 +268,8 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
     const int crank = blockIdx.x % C;
     const int h = blockIdx.x / C, b = blockIdx.y;
     const int k = p.top_k;
+    asp::pdl_wait();
+    asp::pdl_trigger();
     const int len = min(max(seq_lens[b], 0), p.max_seq_len);
     const size_t row_id = (size_t)b * p.n_kv_heads + h;
     const float *row = scores + row_id * p.max_seq_len;
@@ -653,19 +655,6 @@ cudaError_t asp_launch_select(const asp_select_params &p, const float *scores,
         e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
     }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(C * p.n_kv_heads, p.batch);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = C;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, select_kernel, p, scores, seq_lens, sel_idx, dev_flags, C, seg);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
+    return asp_launch(select_kernel, dim3(C * p.n_kv_heads, p.batch), dim3(kThreads), smem, s,
+                      (unsigned)C, p, scores, seq_lens, sel_idx, dev_flags, C, seg);
 }

@@ -31,6 +31,8 @@
 // unsharded scores bit for bit.
 #include <cudaTypedefs.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -227,16 +229,31 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
 #endif
                 tc_fence_after();
                 const uint32_t b_base = bslot0 + bs * C::kBSlotBytes;
+                // descriptors: the start-address field is addr >> 4 in the low
+                // bits (no carry for addresses < 256 KB), so offsets add directly
+                uint64_t adesc[kGroup];
+                uint32_t dcol[kGroup];
 #pragma unroll
-                for (int kk = 0; kk < D / 16; kk++) {
-                    const int r = kk / 4, ko = (kk % 4) * 32;
-                    const uint64_t bdesc = desc_sw128_kmajor(b_base + r * C::kBRegionBytes + ko);
-                    for (int t = 0; t < ng; t++)
-                        mma_bf16_warp(tmem_base + ga[t] * (2 * N) + (kk & 1) * N,
-                                      desc_sw128_kmajor(stage0 + gs[t] * C::kStageBytes +
-                                                        r * (kTileM * 128) + ko),
-                                      bdesc, idesc, kk > 1 ? 1u : 0u);
+                for (int t = 0; t < kGroup; t++) {
+                    adesc[t] = desc_sw128_kmajor(stage0 + gs[t < ng ? t : 0] * C::kStageBytes);
+                    dcol[t] = tmem_base + ga[t < ng ? t : 0] * (2 * N);
                 }
+                const uint64_t bdesc0 = desc_sw128_kmajor(b_base);
+                auto issue = [&](auto NG) {
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; kk++) {
+                        const int r = kk / 4, ko = (kk % 4) * 32;
+                        const uint64_t aoff = (uint64_t)((r * (kTileM * 128) + ko) >> 4);
+                        const uint64_t bdesc = bdesc0 + (uint64_t)((r * C::kBRegionBytes + ko) >> 4);
+#pragma unroll
+                        for (int t = 0; t < decltype(NG)::value; t++)
+                            mma_bf16_warp(dcol[t] + (kk & 1) * N, adesc[t] + aoff, bdesc, idesc,
+                                          kk > 1 ? 1u : 0u);
+                    }
+                };
+                if (ng == kGroup) issue(std::integral_constant<int, kGroup>{});
+                else if (ng == 2) issue(std::integral_constant<int, 2>{});
+                else issue(std::integral_constant<int, 1>{});
                 for (int t = 0; t < ng; t++) {
                     mma_commit_warp(empty_bar(gs[t]));
                     mma_commit_warp(tfull_bar(ga[t]));

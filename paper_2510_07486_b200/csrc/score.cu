@@ -74,6 +74,104 @@ struct Cfg {
                                       kBSlots * kBSlotBytes + 256 /*barriers*/;
 };
 
+// One group of 3 tiles x 8 k-steps (D = 128) in a single asm statement: the
+// operands reach the uniform datapath once and the per-MMA offsets are
+// uniform adds (the A start-address field is addr >> 4; the A tile's two
+// 64-column regions are 16 KB apart, the B operand's N*128 bytes apart).
+__device__ __forceinline__ void mma_group3_d128(uint64_t a0, uint64_t a1, uint64_t a2, uint64_t b0,
+                                                uint32_t d0, uint32_t d1, uint32_t d2,
+                                                uint32_t idesc, uint64_t b_region16,
+                                                uint32_t n_cols) {
+    asm volatile(
+        "{\n\t.reg .pred e, p0, p1;\n\t.reg .b64 ta, tb;\n\t.reg .b32 td;\n\t"
+        "setp.ne.b32 p0, %10, %10;\n\tsetp.eq.b32 p1, %10, %10;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "add.s64 tb, %3, 0;\n\t"
+        "add.s64 ta, %0, 0;\n\t"
+        "mov.u32 td, %4;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p0;\n\t"
+        "add.s64 ta, %1, 0;\n\t"
+        "mov.u32 td, %5;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p0;\n\t"
+        "add.s64 ta, %2, 0;\n\t"
+        "mov.u32 td, %6;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p0;\n\t"
+        "add.s64 tb, %3, 2;\n\t"
+        "add.s64 ta, %0, 2;\n\t"
+        "add.u32 td, %4, %9;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p0;\n\t"
+        "add.s64 ta, %1, 2;\n\t"
+        "add.u32 td, %5, %9;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p0;\n\t"
+        "add.s64 ta, %2, 2;\n\t"
+        "add.u32 td, %6, %9;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p0;\n\t"
+        "add.s64 tb, %3, 4;\n\t"
+        "add.s64 ta, %0, 4;\n\t"
+        "mov.u32 td, %4;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 ta, %1, 4;\n\t"
+        "mov.u32 td, %5;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 ta, %2, 4;\n\t"
+        "mov.u32 td, %6;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 tb, %3, 6;\n\t"
+        "add.s64 ta, %0, 6;\n\t"
+        "add.u32 td, %4, %9;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 ta, %1, 6;\n\t"
+        "add.u32 td, %5, %9;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 ta, %2, 6;\n\t"
+        "add.u32 td, %6, %9;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 tb, %3, %8;\n\tadd.s64 tb, tb, 0;\n\t"
+        "add.s64 ta, %0, 1024;\n\t"
+        "mov.u32 td, %4;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 ta, %1, 1024;\n\t"
+        "mov.u32 td, %5;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 ta, %2, 1024;\n\t"
+        "mov.u32 td, %6;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 tb, %3, %8;\n\tadd.s64 tb, tb, 2;\n\t"
+        "add.s64 ta, %0, 1026;\n\t"
+        "add.u32 td, %4, %9;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 ta, %1, 1026;\n\t"
+        "add.u32 td, %5, %9;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 ta, %2, 1026;\n\t"
+        "add.u32 td, %6, %9;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 tb, %3, %8;\n\tadd.s64 tb, tb, 4;\n\t"
+        "add.s64 ta, %0, 1028;\n\t"
+        "mov.u32 td, %4;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 ta, %1, 1028;\n\t"
+        "mov.u32 td, %5;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 ta, %2, 1028;\n\t"
+        "mov.u32 td, %6;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 tb, %3, %8;\n\tadd.s64 tb, tb, 6;\n\t"
+        "add.s64 ta, %0, 1030;\n\t"
+        "add.u32 td, %4, %9;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 ta, %1, 1030;\n\t"
+        "add.u32 td, %5, %9;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "add.s64 ta, %2, 1030;\n\t"
+        "add.u32 td, %6, %9;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [td], ta, tb, %7, p1;\n\t"
+        "}"
+        ::"l"(a0), "l"(a1), "l"(a2), "l"(b0), "r"(d0), "r"(d1), "r"(d2), "r"(idesc),
+        "l"(b_region16), "r"(n_cols), "r"(0u)
+        : "memory");
+}
+
 struct TileIter {
     long start, end;
     int tpr, n_kv;
@@ -251,7 +349,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
                                           kk > 1 ? 1u : 0u);
                     }
                 };
-                if (ng == kGroup) issue(std::integral_constant<int, kGroup>{});
+                if (D == 128 && ng == 3)
+                    mma_group3_d128(adesc[0], adesc[1], adesc[2], bdesc0, dcol[0], dcol[1], dcol[2],
+                                    idesc, (uint64_t)(C::kBRegionBytes >> 4), (uint32_t)N);
+                else if (ng == kGroup) issue(std::integral_constant<int, kGroup>{});
                 else if (ng == 2) issue(std::integral_constant<int, 2>{});
                 else issue(std::integral_constant<int, 1>{});
                 for (int t = 0; t < ng; t++) {

@@ -108,7 +108,7 @@ asp_status asyncspade_score_select(const asp_select_params *p, const float *q_ha
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = asp_launch_score(*p, q_hat, k_cache, seq_lens, s_buf, dev_flags, s);
     if (e != cudaSuccess) return ASP_ERR_CUDA;
-    return from_cuda(asp_launch_select(*p, s_buf, seq_lens, sel_idx, dev_flags, s));
+    return from_cuda(asp_launch_select(*p, s_buf, seq_lens, sel_idx, dev_flags, scores == nullptr, s));
 }
 
 size_t asyncspade_sparse_decode_workspace(const asp_decode_params *p) {

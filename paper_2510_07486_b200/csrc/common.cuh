@@ -96,9 +96,11 @@ cudaError_t asp_launch_predict(const asp_predict_params &p, const float *q_windo
 cudaError_t asp_launch_score(const asp_select_params &p, const float *q_hat,
                              const asp_bf16 *k_cache, const int32_t *seq_lens, float *scores,
                              uint32_t *dev_flags, cudaStream_t s);
+// discard_scores: the scores live in the caller's workspace and are dead
+// after selection -- their L2 lines are dropped without write-back.
 cudaError_t asp_launch_select(const asp_select_params &p, const float *scores,
                               const int32_t *seq_lens, int32_t *sel_idx, uint32_t *dev_flags,
-                              cudaStream_t s);
+                              bool discard_scores, cudaStream_t s);
 size_t asp_decode_partials_bytes(const asp_decode_params &p);
 cudaError_t asp_launch_decode(const asp_decode_params &p, const asp_bf16 *q,
                               const asp_bf16 *k_cache, const asp_bf16 *v_cache,

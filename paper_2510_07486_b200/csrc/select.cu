@@ -261,7 +261,7 @@ __device__ void cluster_counts(SelectSmem &s, int C, int n, uint32_t *tot, uint3
 __global__ void __launch_bounds__(kThreads, 4)
 select_kernel(asp_select_params p, const float *__restrict__ scores,
               const int32_t *__restrict__ seq_lens, int32_t *__restrict__ sel_idx,
-              uint32_t *dev_flags, int C, int seg_len) {
+              uint32_t *dev_flags, int C, int seg_len, int discard) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SelectSmem &s = *reinterpret_cast<SelectSmem *>(smem_raw);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -629,6 +629,14 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
     nan = __syncthreads_or(nan);
     SPROF(4);
     if (t == 0 && nan) asp::flag_or(dev_flags, ASP_FLAG_NONFINITE);
+    if (discard) {
+        // The scores are dead once selected: drop this segment's L2 lines
+        // without writing them back (only whole 128-B lines inside it).
+        const uintptr_t lo = (reinterpret_cast<uintptr_t>(srow) + 127u) & ~(uintptr_t)127u;
+        const uintptr_t hi = reinterpret_cast<uintptr_t>(srow + n);
+        for (uintptr_t x = lo + (uintptr_t)t * 128u; x + 128u <= hi; x += (uintptr_t)kThreads * 128u)
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(x) : "memory");
+    }
 }
 
 long ceil_div(long a, long b) { return (a + b - 1) / b; }
@@ -637,7 +645,7 @@ long ceil_div(long a, long b) { return (a + b - 1) / b; }
 
 cudaError_t asp_launch_select(const asp_select_params &p, const float *scores,
                               const int32_t *seq_lens, int32_t *sel_idx, uint32_t *dev_flags,
-                              cudaStream_t s) {
+                              bool discard_scores, cudaStream_t s) {
     const long L = p.max_seq_len;
     const long rows = (long)p.batch * p.n_kv_heads;
     // Cluster size: split rows only while they are fewer than the SMs,
@@ -656,5 +664,6 @@ cudaError_t asp_launch_select(const asp_select_params &p, const float *scores,
         if (e != cudaSuccess) return e;
     }
     return asp_launch(select_kernel, dim3(C * p.n_kv_heads, p.batch), dim3(kThreads), smem, s,
-                      (unsigned)C, p, scores, seq_lens, sel_idx, dev_flags, C, seg);
+                      (unsigned)C, p, scores, seq_lens, sel_idx, dev_flags, C, seg,
+                      discard_scores ? 1 : 0);
 }

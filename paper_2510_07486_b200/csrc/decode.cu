@@ -469,6 +469,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                 mbar_arrive(bar(B_TOKEMPTY + slot));
             }
         };
+        const uint64_t keep = l2_policy_evict_last();
         auto epilogue = [&](int i) {
             const int slot = i & 1;
             const uint32_t use = (uint32_t)((i >> 1) & 1);
@@ -485,14 +486,18 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             const int d = quad * 32 + lane;
 #pragma unroll
             for (int g = 0; g < G; g++) {
+                // partials are read back by the combine kernel right after:
+                // keep them in L2 (it drops them once merged)
                 float *dst = partials + (((size_t)b * Hq + h * G + g) * n_splits + it.chunk) * (D + 2);
-                if (d < D) dst[2 + d] = __fadd_rn(__uint_as_float(r[g]), __uint_as_float(r[G + g]));
+                if (d < D)
+                    st_global_hint(dst + 2 + d,
+                                   __fadd_rn(__uint_as_float(r[g]), __uint_as_float(r[G + g])), keep);
                 if (d == 0) {
                     float L = 0.0f;
 #pragma unroll
                     for (int w = 0; w < 4; w++) L += s_wsum[(slot * 4 + w) * 8 + g];
-                    dst[0] = s_mrow[slot * 8 + g];
-                    dst[1] = L;
+                    st_global_hint(dst, s_mrow[slot * 8 + g], keep);
+                    st_global_hint(dst + 1, L, keep);
                 }
             }
         };
@@ -530,6 +535,13 @@ decode_combine_kernel(asp_decode_params p, const float *__restrict__ partials,
         }
     }
     out[((size_t)b * p.n_q_heads + hq) * D + d] = (L > 0.0f) ? O / L : 0.0f;
+    // the partials are dead once merged: drop their L2 lines without write-back
+    // (whole 128-B lines inside this (b, hq) block only)
+    __syncthreads();
+    const uintptr_t lo = (reinterpret_cast<uintptr_t>(src) + 127u) & ~(uintptr_t)127u;
+    const uintptr_t hi = reinterpret_cast<uintptr_t>(src + (size_t)n_splits * (D + 2));
+    for (uintptr_t x = lo + (uintptr_t)d * 128u; x + 128u <= hi; x += (uintptr_t)D * 128u)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(x) : "memory");
 }
 
 int n_splits_of(const asp_decode_params &p) {

@@ -196,7 +196,7 @@ def run_reference(args, cfg):
 def main():
     args = _args()
     from paper_2510_07486_b200 import configs
-    cfg = {c.name: c for c in (configs.TINY, configs.QWEN3_8B, configs.QWEN3_32B)}[args.config]
+    cfg = configs.by_name(args.config)
     if args.impl == "reference":
         return run_reference(args, cfg)
 

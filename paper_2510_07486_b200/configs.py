@@ -44,3 +44,15 @@ def high_concurrency(batch: int) -> Config:
 
 
 BY_NAME = {c.name: c for c in (TINY, QWEN3_8B, QWEN3_32B)}
+
+
+def by_name(name: str) -> Config:
+    """A config by name: the three fixed ones, or a sweep point such as
+    'long-cot_b8_ctx524288' / 'high-conc_b512_ctx4k' (configs [3], [4])."""
+    if name in BY_NAME:
+        return BY_NAME[name]
+    if name.startswith("long-cot_b8_ctx"):
+        return long_cot(int(name.rsplit("ctx", 1)[1]))
+    if name.startswith("high-conc_b") and name.endswith("_ctx4k"):
+        return high_concurrency(int(name[len("high-conc_b"):-len("_ctx4k")]))
+    raise KeyError(f"unknown config {name!r}")

@@ -42,6 +42,9 @@ def _args():
     ap.add_argument("--config", default="qwen3-32b_b64_ctx32k")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--emulate-shard", type=int, default=0, metavar="P",
+                    help="one GPU runs rank 0's shard of a P-way KV-head split (the per-GPU "
+                         "work of the P-GPU run; scaling evidence when only one GPU is at hand)")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: skip clocks, e2e and the CPU baseline")
     return ap.parse_args()
@@ -214,7 +217,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2510_07486_b200.shard import kv_head_shard
-    h0, hn = kv_head_shard(cfg.n_kv_heads, world, rank)     # §8(e): KV-head sharding
+    shards = args.emulate_shard if (args.emulate_shard and world == 1) else world
+    h0, hn = kv_head_shard(cfg.n_kv_heads, shards, rank)    # §8(e): KV-head sharding
     step = DecodeStep(cfg, "cuda", kv_heads=(h0, hn))
     step.fill_synthetic()
     torch.cuda.synchronize()
@@ -378,7 +382,8 @@ def main():
             "config": {"workload": cfg.name, "batch": cfg.batch, "n_q_heads": cfg.n_q_heads,
                        "n_kv_heads": cfg.n_kv_heads, "head_dim": cfg.head_dim,
                        "seq_len": cfg.seq_len, "top_k": cfg.top_k, "window": cfg.window,
-                       "parallelism": f"kv-head shard x{world}",
+                       "parallelism": f"kv-head shard x{world}" if shards == world else
+                                      f"emulated: rank 0 of a {shards}-way kv-head shard on 1 GPU",
                        "l2": "no flush: K+V per GPU (%.2f GB) >> 126 MB L2" %
                              (2 * k_bytes / 1e9)},
             "hbm_tb_per_s": core / (ms_step * 1e-3) / 1e12,

@@ -407,6 +407,278 @@ predict_kernel(asp_predict_params p, const float *__restrict__ q_window,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Fast path for the common case (2 <= W <= 16, masked-shared or single-window
+// assembly): TWO rows per warp.  The W x W Gram of both rows runs on the fp64
+// tensor cores from 128-bit loads (the contraction index d is permuted
+// identically in both operands, so each lane's float4 feeds four k-steps and
+// the two rows give six independent accumulator chains); then each half-warp
+// owns one row for the branch-free register Gauss-Jordan solve (lane l = row l
+// of [G0 + eps I | beta], padded to 16 with identity rows that change
+// nothing), the shuffle-only masked-shared coefficient assembly and the
+// weighted sum -- so every instruction of the sequential part serves two
+// rows.  Non-finite windows are caught by the Gram diagonal (sum of squares:
+// finite iff every element is) instead of a per-element test.
+ASP_DEV double rcp_nr(double d) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    double e = fma(-d, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-d, y, 1.0);
+    return fma(y, e, y);
+}
+
+ASP_DEV double shfl16(double v, int src) { return __shfl_sync(0xffffffffu, v, src, 16); }
+ASP_DEV double shfl16_up(double v, unsigned dl) { return __shfl_up_sync(0xffffffffu, v, dl, 16); }
+ASP_DEV double half_max(double v) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o, 16));
+    return v;
+}
+ASP_DEV double half_sum(double v) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, 16);
+    return v;
+}
+// softmax over lanes l < n of the half-warp (0 beyond n)
+ASP_DEV double half_softmax(double v, int l, int n) {
+    const double m = half_max(l < n ? v : -INFINITY);
+    const double e = l < n ? exp(v - m) : 0.0;
+    return e / half_sum(e);
+}
+
+constexpr int kPairWarps = 8;
+constexpr int kGS = 17;                            // smem row stride of a Gram (doubles)
+
+template <int D, int NB>
+__global__ void __launch_bounds__(kPairWarps * 32)
+predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
+                    float *__restrict__ q_hat, uint32_t *dev_flags) {
+    extern __shared__ double sG_raw[];
+    double (*sG)[2][16 * kGS] = reinterpret_cast<double (*)[2][16 * kGS]>(sG_raw);
+    const int W = p.window, n = W - 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long rows = (long)p.batch * p.n_q_heads;
+    const long row0 = ((long)blockIdx.x * (blockDim.x >> 5) + warp) * 2;
+    asp::pdl_wait();
+    asp::pdl_trigger();
+    if (row0 >= rows) return;
+    const bool has1 = row0 + 1 < rows;
+    const int rs = p.ring_start;
+#ifdef ASP_PROFILE_PREDICT
+    long long _tp = clock64();
+#endif
+    auto phys_of = [&](int i) {
+        const int ph = i + rs;
+        return ph >= W ? ph - W : ph;
+    };
+
+    // ---- Step 2: augmented Gram G' = Q Q^T of both rows, fp64 MMA.
+    {
+        const int fr = lane >> 2, fc = lane & 3;
+        constexpr int T = NB * (NB + 1) / 2;
+        double acc[2][T][2];
+#pragma unroll
+        for (int r = 0; r < 2; r++)
+#pragma unroll
+            for (int t = 0; t < T; t++) acc[r][t][0] = acc[r][t][1] = 0.0;
+        const float4 *rp[2][NB];
+#pragma unroll
+        for (int r = 0; r < 2; r++)
+#pragma unroll
+            for (int b = 0; b < NB; b++) {
+                const int i = 8 * b + fr;
+                const bool live = i < W && (r == 0 || has1);
+                rp[r][b] = live ? reinterpret_cast<const float4 *>(
+                                      q_window + (size_t)(row0 + r) * W * D + (size_t)phys_of(i) * D) + fc
+                                : nullptr;
+            }
+#pragma unroll 2
+        for (int s = 0; s < D / 16; s++) {
+            float4 f[2][NB];
+#pragma unroll
+            for (int r = 0; r < 2; r++)
+#pragma unroll
+                for (int b = 0; b < NB; b++)
+                    f[r][b] = rp[r][b] ? __ldg(rp[r][b] + 4 * s) : make_float4(0.f, 0.f, 0.f, 0.f);
+            // k-step j of group s pairs d = 16 s + 4 fc + j in both operands
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+#pragma unroll
+                for (int r = 0; r < 2; r++) {
+                    int t = 0;
+#pragma unroll
+                    for (int bi = 0; bi < NB; bi++)
+#pragma unroll
+                        for (int bj = bi; bj < NB; bj++, t++) {
+                            const float a = j == 0 ? f[r][bi].x : j == 1 ? f[r][bi].y : j == 2 ? f[r][bi].z : f[r][bi].w;
+                            const float b = j == 0 ? f[r][bj].x : j == 1 ? f[r][bj].y : j == 2 ? f[r][bj].z : f[r][bj].w;
+                            dmma(acc[r][t][0], acc[r][t][1], (double)a, (double)b);
+                        }
+                }
+        }
+        // lane holds C[8 bi + fr][8 bj + 2 fc + e]
+#pragma unroll
+        for (int r = 0; r < 2; r++) {
+            int t = 0;
+#pragma unroll
+            for (int bi = 0; bi < NB; bi++)
+#pragma unroll
+                for (int bj = bi; bj < NB; bj++, t++)
+#pragma unroll
+                    for (int e = 0; e < 2; e++) {
+                        const int i = 8 * bi + fr, j = 8 * bj + 2 * fc + e;
+                        if (i < W && j < W) {
+                            sG[warp][r][i * kGS + j] = acc[r][t][e];
+                            sG[warp][r][j * kGS + i] = acc[r][t][e];
+                        }
+                    }
+        }
+    }
+    __syncwarp();
+    PPROF(0);
+
+    // ---- from here each half-warp owns one row: h = row, l = lane within the half
+    const int h = lane >> 4, l = lane & 15;
+    const unsigned hmask = 0xFFFFu << (16 * h);
+    const double *G = sG[warp][h];
+    const bool own = l < n;
+    const double gdiag = l < W ? G[l * kGS + l] : 0.0;
+    const bool finite = (__ballot_sync(0xffffffffu, isfinite(gdiag)) & hmask) == hmask;
+
+    // ---- Step 3: omega = (G0 + eps I)^{-1} beta, Gauss-Jordan in registers.
+    double tr = half_sum(own && finite ? gdiag : 0.0);
+    double e = (p.flags & ASP_EPS_ABSOLUTE) ? (double)p.eps : (double)p.eps * (tr / n);
+    if (e == 0.0) e = 1e-30;                                           // reading R7
+    // (a non-finite window solves the identity system instead, so no NaN or
+    // inf flows through the shared arithmetic below; its output is the
+    // passthrough either way)
+    const bool sys = own && finite;
+    double r[16];
+#pragma unroll
+    for (int k = 0; k < 16; k++)
+        r[k] = sys ? (k < n ? G[l * kGS + k] + (k == l ? e : 0.0) : 0.0) : (k == l ? 1.0 : 0.0);
+    double rb = sys ? G[n * kGS + l] : 0.0;                             // beta_l = (H y)_l
+    bool pd = true;
+    double diag = 1.0;
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+        const double d = shfl16(r[j], j);
+        const double pb = shfl16(rb, j);
+        const bool good = d > 0.0 && d < INFINITY;                     // SPD: pivots > 0
+        pd = pd && good;
+        const double f = l != j ? r[j] * rcp_nr(good ? d : 1.0) : 0.0;  // the pivot row stays
+        diag = l == j ? d : diag;
+#pragma unroll
+        for (int k = j + 1; k < 16; k++) r[k] = fma(-f, shfl16(r[k], j), r[k]);
+        rb = fma(-f, pb, rb);
+    }
+    const double x = own ? rb * rcp_nr(diag) : 0.0;
+    // (the ballot runs on every lane: never behind a short-circuit)
+    const unsigned solved = __ballot_sync(0xffffffffu, pd && (!own || isfinite(x)));
+    const bool ok = finite && (solved & hmask) == hmask;
+    PPROF(1);
+
+    // ---- Steps 4-6: coefficients c_p of q_hat = sum_p c_p Q[p] / m;
+    // lane l holds c_{l+1} (c_0 = 0 in both assemblies).
+    const double sgn = (p.flags & ASP_SIGN_NEGATED) ? -1.0 : 1.0;
+    const uint32_t mode = p.flags & 0xFu;
+    double c = 0.0, denom = 1.0;
+    if (mode == ASP_ASSEMBLY_SINGLE) {
+        // Eq. 4: omega[i] (history row i) weights Q[i+1].
+        const double w = (p.flags & ASP_NORM_NONE) ? x : half_softmax(sgn * x, l, n);
+        c = own ? w : 0.0;
+    } else {
+        // masked-shared (readings R4-R6): row j = 1..W uses softmax(v[0..n_j)),
+        // n_j = min(j, n), on the newest n_j queries; rows W-1 and W share n_j = n.
+        double v = sgn * x;
+        if (p.flags & ASP_DOUBLE_SOFTMAX) v = half_softmax(v, l, n);    // literal Step 3
+        const double m = half_max(own ? v : -INFINITY);
+        const double ev = own ? exp(v - m) : 0.0;
+        double S = ev;                                                // inclusive prefix: S_{l+1}
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+            const double t = shfl16_up(S, o);
+            if (l >= o) S += t;
+        }
+        const double invS = rcp_nr(S > 0.0 ? S : 1.0);
+        const bool tiny = (__ballot_sync(0xffffffffu, l == 0 && !(S > 1e-280)) & hmask) != 0;
+        const bool tiny_any = __any_sync(0xffffffffu, tiny);           // warp-uniform
+#pragma unroll
+        for (int mm = 1; mm < 16; mm++) {
+            if (mm > n) break;                                        // n is warp-uniform
+            const unsigned sh = (unsigned)(n - mm);
+            double t = ev * shfl16(invS, mm - 1);
+            if (tiny_any) {
+                // a prefix's exponentials underflowed against the global max:
+                // this prefix's own max
+                const double mx = half_max(l < mm ? v : -INFINITY);
+                const double ex = l < mm ? exp(v - mx) : 0.0;
+                const double ts = ex / half_sum(ex);
+                if (tiny) t = ts;
+            }
+            if (mm == n) t *= 2.0;
+            const double u = shfl16_up(t, sh);
+            if (l >= (int)sh && own) c += u;
+        }
+        denom = (double)W;
+    }
+
+    PPROF(2);
+    // ---- q_hat = (1/m) sum_p c_p Q[p] (one pass over the cache-hot window), or
+    // the passthrough Q_t.
+    const bool live = h == 0 || has1;
+    const float *src = q_window + (size_t)(row0 + h) * W * D;
+    float *out = q_hat + (size_t)(row0 + h) * D;
+    constexpr int kV = D / 64;                                          // float4 per lane
+    // (all lanes run the loop -- its shuffles span both halves -- even when a
+    // half falls back to the passthrough)
+    double acc[kV][4];
+#pragma unroll
+    for (int u = 0; u < kV; u++) acc[u][0] = acc[u][1] = acc[u][2] = acc[u][3] = 0.0;
+    for (int q = 1; q < W; q++) {
+        const double cq = shfl16(c, q - 1);
+        const float4 *rq = reinterpret_cast<const float4 *>(src + (size_t)phys_of(q) * D) + l;
+#pragma unroll
+        for (int u = 0; u < kV; u++) {
+            const float4 v4 = live ? __ldg(rq + 16 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+            acc[u][0] = fma(cq, (double)v4.x, acc[u][0]);
+            acc[u][1] = fma(cq, (double)v4.y, acc[u][1]);
+            acc[u][2] = fma(cq, (double)v4.z, acc[u][2]);
+            acc[u][3] = fma(cq, (double)v4.w, acc[u][3]);
+        }
+    }
+    if (live && ok) {
+        const double inv_m = 1.0 / denom;
+#pragma unroll
+        for (int u = 0; u < kV; u++)
+            reinterpret_cast<float4 *>(out)[l + 16 * u] =
+                make_float4((float)(acc[u][0] * inv_m), (float)(acc[u][1] * inv_m),
+                            (float)(acc[u][2] * inv_m), (float)(acc[u][3] * inv_m));
+    } else if (live) {
+        const float4 *rq = reinterpret_cast<const float4 *>(src + (size_t)phys_of(W - 1) * D) + l;
+#pragma unroll
+        for (int u = 0; u < kV; u++) reinterpret_cast<float4 *>(out)[l + 16 * u] = rq[16 * u];
+        if (l == 0) asp::flag_or(dev_flags, finite ? ASP_FLAG_NOT_PD : ASP_FLAG_NONFINITE);
+    }
+    PPROF(3);
+}
+
+template <int D, int NB>
+cudaError_t launch_pair(const asp_predict_params &p, const float *q_window, float *q_hat,
+                        uint32_t *dev_flags, cudaStream_t s) {
+    const long rows = (long)p.batch * p.n_q_heads;
+    const long warps = (rows + 1) / 2;
+    // as many CTAs as it takes to cover the SMs twice before packing 8 warps each
+    const long target = 2L * asp_sm_count();
+    int wpc = 1;
+    while (wpc < kPairWarps && (warps + 2 * wpc - 1) / (2 * wpc) >= target) wpc *= 2;
+    const unsigned grid = (unsigned)((warps + wpc - 1) / wpc);
+    const size_t smem = (size_t)wpc * 2 * 16 * kGS * sizeof(double);
+    return asp_launch(predict_pair_kernel<D, NB>, dim3(grid), dim3(wpc * 32), smem, s, 1, p,
+                      q_window, q_hat, dev_flags);
+}
+
 template <int D, int NB>
 cudaError_t launch(const asp_predict_params &p, const float *q_window, float *q_hat,
                    uint32_t *dev_flags, cudaStream_t s) {
@@ -427,6 +699,14 @@ cudaError_t launch(const asp_predict_params &p, const float *q_window, float *q_
 cudaError_t asp_launch_predict(const asp_predict_params &p, const float *q_window, float *q_hat,
                                uint32_t *dev_flags, cudaStream_t s) {
     const int nb = (p.window + 7) / 8;
+    const uint32_t mode = p.flags & 0xFu;
+    if (p.window >= 2 && p.window <= 16 &&
+        (mode == ASP_ASSEMBLY_MASKED_SHARED || mode == ASP_ASSEMBLY_SINGLE)) {
+        if (p.head_dim == 64) return nb == 1 ? launch_pair<64, 1>(p, q_window, q_hat, dev_flags, s)
+                                             : launch_pair<64, 2>(p, q_window, q_hat, dev_flags, s);
+        if (p.head_dim == 128) return nb == 1 ? launch_pair<128, 1>(p, q_window, q_hat, dev_flags, s)
+                                              : launch_pair<128, 2>(p, q_window, q_hat, dev_flags, s);
+    }
 #define ASP_CASE(DD, NBB) \
     if (p.head_dim == DD && nb == NBB) return launch<DD, NBB>(p, q_window, q_hat, dev_flags, s);
     ASP_CASE(64, 1) ASP_CASE(64, 2) ASP_CASE(64, 3) ASP_CASE(64, 4)

@@ -56,7 +56,8 @@ PRED_FLAGS = [0, asp.ASSEMBLY_SINGLE, asp.ASSEMBLY_PER_WINDOW, asp.DOUBLE_SOFTMA
 
 
 @pytest.mark.parametrize("flags", PRED_FLAGS)
-@pytest.mark.parametrize("shape", [(1, 2, 4, 64), (32, 32, 16, 128), (3, 5, 32, 64), (2, 3, 2, 128)])
+@pytest.mark.parametrize("shape", [(1, 2, 4, 64), (32, 32, 16, 128), (3, 5, 32, 64), (2, 3, 2, 128),
+                                   (3, 5, 9, 128), (1, 3, 8, 64), (7, 3, 17, 128)])
 def test_predict_parity(flags, shape):
     B, Hq, W, D = shape
     win, _ = synth.query_trace(synth.base_seed(1) + W, B, Hq, W, D)

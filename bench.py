@@ -42,6 +42,8 @@ def _args():
     ap.add_argument("--config", default="qwen3-32b_b64_ctx32k")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-a5", action="store_true",
+                    help="skip the a5 (asynchronous selection) pipelined measurement")
     ap.add_argument("--emulate-shard", type=int, default=0, metavar="P",
                     help="one GPU runs rank 0's shard of a P-way KV-head split (the per-GPU "
                          "work of the P-GPU run; scaling evidence when only one GPU is at hand)")
@@ -369,6 +371,41 @@ def main():
                "d2h_bytes_per_step": bo * world,
                "copies": "pinned host, copy stream, double-buffered, overlapped with compute"}
 
+    # a5: the paper's steady state -- selection
+    # for step t+1 (predict, score, top-k) on a side stream, overlapped with
+    # step t's sparse attention on the main stream; the same four kernels per
+    # step, reported beside the serial headline (no synthetic forward here).
+    a5 = None
+    if not (args.no_a5 or args.profile):
+        from paper_2510_07486_b200.pipeline import AsyncPipeline
+        del step
+        torch.cuda.empty_cache()
+        st1 = DecodeStep(cfg, "cuda", kv_heads=(h0, hn), n_fresh=1)
+        st1.fill_synthetic()
+        pipe = AsyncPipeline(st1)
+        res = {}
+        for name, fn in (("serial", pipe.run_step_serial), ("pipelined", pipe.run_step)):
+            for _ in range(3):
+                fn()
+            pipe.drain()
+            barrier()
+            e0, e1 = ev(), ev()
+            e0.record(stream)
+            for _ in range(args.steps):
+                fn()
+            pipe.drain()
+            e1.record(stream)
+            barrier()
+            tt = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            res[name] = float(tt[0]) * 1e3
+        a5 = {"serial_us": res["serial"], "pipelined_us": res["pipelined"], "unit": UNIT,
+              "what": "steady-state step with selection for t+1 on a side stream overlapped "
+                      "with decode(t) (n_fresh = 1); serial = the same calls on one stream"}
+        del pipe, st1
+        torch.cuda.empty_cache()
+
     if rank == 0:
         peak, peak_src = _peaks()
         core = cfg.core_bytes(hn)                      # per GPU
@@ -405,6 +442,8 @@ def main():
             line["allgather_out_ms"] = gather_ms
         if e2e is not None:
             line["e2e"] = e2e
+        if a5 is not None:
+            line["a5"] = a5
         if world == 1 and not (args.no_cpu_baseline or args.profile):
             line["cpu_baseline"] = cpu_baseline(cfg)
         print(json.dumps(line), flush=True)

@@ -428,6 +428,13 @@ ASP_DEV double rcp_nr(double d) {
     return fma(y, e, y);
 }
 
+// one Newton step: relative error ~2^-44 (the pivots of the elimination)
+ASP_DEV double rcp_nr1(double d) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    return fma(y, fma(-d, y, 1.0), y);
+}
+
 ASP_DEV double shfl16(double v, int src) { return __shfl_sync(0xffffffffu, v, src, 16); }
 ASP_DEV double shfl16_up(double v, unsigned dl) { return __shfl_up_sync(0xffffffffu, v, dl, 16); }
 ASP_DEV double half_max(double v) {
@@ -477,11 +484,11 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
     {
         const int fr = lane >> 2, fc = lane & 3;
         constexpr int T = NB * (NB + 1) / 2;
-        double acc[2][T][2];
+        double acc[2][T][2], acc2[2][T][2];             // even / odd groups: shorter chains
 #pragma unroll
         for (int r = 0; r < 2; r++)
 #pragma unroll
-            for (int t = 0; t < T; t++) acc[r][t][0] = acc[r][t][1] = 0.0;
+            for (int t = 0; t < T; t++) acc[r][t][0] = acc[r][t][1] = acc2[r][t][0] = acc2[r][t][1] = 0.0;
         const float4 *rp[2][NB];
 #pragma unroll
         for (int r = 0; r < 2; r++)
@@ -493,30 +500,43 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
                                       q_window + (size_t)(row0 + r) * W * D + (size_t)phys_of(i) * D) + fc
                                 : nullptr;
             }
-#pragma unroll 2
-        for (int s = 0; s < D / 16; s++) {
-            float4 f[2][NB];
+#pragma unroll 1
+        for (int s = 0; s < D / 16; s += 2) {
+            float4 f[2][2][NB];
 #pragma unroll
-            for (int r = 0; r < 2; r++)
+            for (int hh = 0; hh < 2; hh++)
 #pragma unroll
-                for (int b = 0; b < NB; b++)
-                    f[r][b] = rp[r][b] ? __ldg(rp[r][b] + 4 * s) : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int r = 0; r < 2; r++)
+#pragma unroll
+                    for (int b = 0; b < NB; b++)
+                        f[hh][r][b] = rp[r][b] ? __ldg(rp[r][b] + 4 * (s + hh)) : make_float4(0.f, 0.f, 0.f, 0.f);
             // k-step j of group s pairs d = 16 s + 4 fc + j in both operands
 #pragma unroll
             for (int j = 0; j < 4; j++)
 #pragma unroll
-                for (int r = 0; r < 2; r++) {
-                    int t = 0;
+                for (int hh = 0; hh < 2; hh++)
 #pragma unroll
-                    for (int bi = 0; bi < NB; bi++)
+                    for (int r = 0; r < 2; r++) {
+                        int t = 0;
 #pragma unroll
-                        for (int bj = bi; bj < NB; bj++, t++) {
-                            const float a = j == 0 ? f[r][bi].x : j == 1 ? f[r][bi].y : j == 2 ? f[r][bi].z : f[r][bi].w;
-                            const float b = j == 0 ? f[r][bj].x : j == 1 ? f[r][bj].y : j == 2 ? f[r][bj].z : f[r][bj].w;
-                            dmma(acc[r][t][0], acc[r][t][1], (double)a, (double)b);
-                        }
-                }
+                        for (int bi = 0; bi < NB; bi++)
+#pragma unroll
+                            for (int bj = bi; bj < NB; bj++, t++) {
+                                const float4 &A = f[hh][r][bi], &B = f[hh][r][bj];
+                                const float a = j == 0 ? A.x : j == 1 ? A.y : j == 2 ? A.z : A.w;
+                                const float b = j == 0 ? B.x : j == 1 ? B.y : j == 2 ? B.z : B.w;
+                                double *c = hh ? acc2[r][t] : acc[r][t];
+                                dmma(c[0], c[1], (double)a, (double)b);
+                            }
+                    }
         }
+#pragma unroll
+        for (int r = 0; r < 2; r++)
+#pragma unroll
+            for (int t = 0; t < T; t++) {
+                acc[r][t][0] += acc2[r][t][0];
+                acc[r][t][1] += acc2[r][t][1];
+            }
         // lane holds C[8 bi + fr][8 bj + 2 fc + e]
 #pragma unroll
         for (int r = 0; r < 2; r++) {
@@ -567,7 +587,7 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
         const double pb = shfl16(rb, j);
         const bool good = d > 0.0 && d < INFINITY;                     // SPD: pivots > 0
         pd = pd && good;
-        const double f = l != j ? r[j] * rcp_nr(good ? d : 1.0) : 0.0;  // the pivot row stays
+        const double f = l != j ? r[j] * rcp_nr1(good ? d : 1.0) : 0.0; // the pivot row stays
         diag = l == j ? d : diag;
 #pragma unroll
         for (int k = j + 1; k < 16; k++) r[k] = fma(-f, shfl16(r[k], j), r[k]);
@@ -604,6 +624,7 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
         const double invS = rcp_nr(S > 0.0 ? S : 1.0);
         const bool tiny = (__ballot_sync(0xffffffffu, l == 0 && !(S > 1e-280)) & hmask) != 0;
         const bool tiny_any = __any_sync(0xffffffffu, tiny);           // warp-uniform
+        double c2 = 0.0;
 #pragma unroll
         for (int mm = 1; mm < 16; mm++) {
             if (mm > n) break;                                        // n is warp-uniform
@@ -619,8 +640,12 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
             }
             if (mm == n) t *= 2.0;
             const double u = shfl16_up(t, sh);
-            if (l >= (int)sh && own) c += u;
+            if (l >= (int)sh && own) {
+                if (mm & 1) c += u;
+                else c2 += u;
+            }
         }
+        c += c2;
         denom = (double)W;
     }
 
@@ -633,21 +658,33 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
     constexpr int kV = D / 64;                                          // float4 per lane
     // (all lanes run the loop -- its shuffles span both halves -- even when a
     // half falls back to the passthrough)
-    double acc[kV][4];
+    double acc[kV][4], acc2[kV][4];
 #pragma unroll
-    for (int u = 0; u < kV; u++) acc[u][0] = acc[u][1] = acc[u][2] = acc[u][3] = 0.0;
-    for (int q = 1; q < W; q++) {
+    for (int u = 0; u < kV; u++)
+#pragma unroll
+        for (int z = 0; z < 4; z++) acc[u][z] = acc2[u][z] = 0.0;
+    auto axpy = [&](double (&a)[kV][4], int q) {
         const double cq = shfl16(c, q - 1);
         const float4 *rq = reinterpret_cast<const float4 *>(src + (size_t)phys_of(q) * D) + l;
 #pragma unroll
         for (int u = 0; u < kV; u++) {
             const float4 v4 = live ? __ldg(rq + 16 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
-            acc[u][0] = fma(cq, (double)v4.x, acc[u][0]);
-            acc[u][1] = fma(cq, (double)v4.y, acc[u][1]);
-            acc[u][2] = fma(cq, (double)v4.z, acc[u][2]);
-            acc[u][3] = fma(cq, (double)v4.w, acc[u][3]);
+            a[u][0] = fma(cq, (double)v4.x, a[u][0]);
+            a[u][1] = fma(cq, (double)v4.y, a[u][1]);
+            a[u][2] = fma(cq, (double)v4.z, a[u][2]);
+            a[u][3] = fma(cq, (double)v4.w, a[u][3]);
         }
+    };
+    int q = 1;
+    for (; q + 1 < W; q += 2) {
+        axpy(acc, q);
+        axpy(acc2, q + 1);
     }
+    if (q < W) axpy(acc, q);
+#pragma unroll
+    for (int u = 0; u < kV; u++)
+#pragma unroll
+        for (int z = 0; z < 4; z++) acc[u][z] += acc2[u][z];
     if (live && ok) {
         const double inv_m = 1.0 / denom;
 #pragma unroll

@@ -5,6 +5,13 @@ KV-head-sharded) layer and runs a1 -> a2+a3 -> a4 through the C ABI
 (predict_query, score_select, sparse_decode), optionally replayed as a CUDA
 graph.  torch is used only to allocate memory and provide the stream.
 
+Layer packing (the paper's depth-wise parallelism,
+P:247-249): with `layers = P_l` the buffers of P_l consecutive layers are
+stacked along the batch axis ([P_l * B, ...], layer-major), so ONE launch of
+each kernel predicts, scores, selects and attends for all P_l layers -- the
+predicted queries of every layer are available together, and every row is
+independent, so a packed step reproduces the per-layer steps bit for bit.
+
 Sharding (§8(e) of SURVEY.md): a shard owns KV heads
 [h0, h0 + n_kv_heads) and the matching q heads for every batch row.  Every
 kernel's per-row arithmetic depends only on the row, so a shard reproduces
@@ -22,14 +29,17 @@ from .configs import Config
 
 class DecodeStep:
     def __init__(self, cfg: Config, device="cuda", *, kv_heads: tuple[int, int] | None = None,
-                 n_fresh: int = 0, eps: float = 1e-2, flags: int = 0, keep_scores: bool = False):
+                 n_fresh: int = 0, eps: float = 1e-2, flags: int = 0, keep_scores: bool = False,
+                 layers: int = 1):
         self.cfg = cfg
+        self.layers = layers
         self.device = torch.device(device)
         h0, hn = kv_heads if kv_heads is not None else (0, cfg.n_kv_heads)
         self.h0, self.n_kv = h0, hn
         G = cfg.group
         self.q0, self.n_q = h0 * G, hn * G
-        B, W, D, L = cfg.batch, cfg.window, cfg.head_dim, cfg.seq_len
+        W, D, L = cfg.window, cfg.head_dim, cfg.seq_len
+        B = cfg.batch * layers                     # layer-major packing along the batch axis
         dev = self.device
         self.n_fresh, self.eps, self.flags = n_fresh, eps, flags
         self.ring_start = 0
@@ -59,10 +69,14 @@ class DecodeStep:
         values of global heads [h0, h0+n) -- identical on any sharding."""
         cfg = self.cfg
         seed = synth.base_seed(cfg.index) if seed is None else seed
-        synth.fill_kv_device(self.k_cache, seed, synth.STREAM_K, 0, self.h0, cfg.n_kv_heads)
-        synth.fill_kv_device(self.v_cache, seed, synth.STREAM_V, 0, self.h0, cfg.n_kv_heads)
-        synth.fill_query_device(self.window, self.q.view(torch.int16), seed, 0, self.q0,
-                                cfg.n_q_heads)
+        B = cfg.batch
+        for layer in range(self.layers):
+            sd = seed + synth.LAYER_SEED_STRIDE * layer
+            rows = slice(layer * B, (layer + 1) * B)
+            synth.fill_kv_device(self.k_cache[rows], sd, synth.STREAM_K, 0, self.h0, cfg.n_kv_heads)
+            synth.fill_kv_device(self.v_cache[rows], sd, synth.STREAM_V, 0, self.h0, cfg.n_kv_heads)
+            synth.fill_query_device(self.window[rows], self.q[rows].view(torch.int16), sd, 0,
+                                    self.q0, cfg.n_q_heads)
         self.ring_start = 0
         self.p_pred.ring_start = 0
 

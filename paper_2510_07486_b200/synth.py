@@ -32,6 +32,9 @@ AR_ALPHA = np.float32(0.95)
 AR_SIGMA = np.float32(0.05)
 
 
+# layer l of a layer-packed step uses seed + LAYER_SEED_STRIDE * l
+LAYER_SEED_STRIDE = 7919
+
 def base_seed(config_index: int, repetition: int = 0) -> int:
     """seed = 20251008 + 1000 * config_index + repetition."""
     return 20251008 + 1000 * config_index + repetition

@@ -6,7 +6,8 @@ os.environ["ASYNCSPADE_LIB"] = os.path.join(os.path.dirname(os.path.dirname(os.p
 import paper_2510_07486_b200 as asp
 from paper_2510_07486_b200 import configs
 from paper_2510_07486_b200.step import DecodeStep
-step = DecodeStep(configs.QWEN3_32B, "cuda")
+P = int(os.environ.get("SHARD", "1"))
+step = DecodeStep(configs.QWEN3_32B, "cuda", kv_heads=(0, 8 // P))
 step.fill_synthetic()
 asp.predict_query(step.window, step.q_hat, params=step.p_pred)
 L = asp.lib()
@@ -17,7 +18,7 @@ for it in range(3):
     torch.cuda.synchronize()
 L.asp_select_prof_read(buf)
 names = ["sample", "bracket", "classify", "radix", "emit"]
-rows = 512
+rows = 512 // P
 for n, v in zip(names, buf):
     print(f"{n:12s} {v / rows / 1.93e3:8.2f} us/row")
 print("candidates per CTA", buf[6] / rows, " fallback CTAs", buf[7])

@@ -2,6 +2,7 @@
 
     python scripts/sweep.py long-cot          # [3] batch 8, ctx 4k..512k, per-GPU shard of P = 8
     python scripts/sweep.py high-concurrency  # [4] Qwen3-8B shape, ctx 4k, batch 1..512, a5 overlap
+    python scripts/sweep.py layer-packed      # NEXT-2: P_l layers per launch (small shapes)
 
 One JSON line per point.  Times are CUDA events on the launching stream over
 `--steps` back-to-back steps after `--warmup`, per step in µs.  Core bytes as
@@ -98,7 +99,7 @@ def point(cfg, args, kv_heads=None, overlap=False):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("sweep", choices=["long-cot", "high-concurrency"])
+    ap.add_argument("sweep", choices=["long-cot", "high-concurrency", "layer-packed"])
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--out", default=None)
@@ -110,6 +111,23 @@ def main():
             cfg = configs.long_cot(1 << e)
             lines.append(point(cfg, args, kv_heads=(0, 1)))     # per-GPU shard at P = 8
             print(json.dumps(lines[-1]), flush=True)
+    elif args.sweep == "layer-packed":
+        # NEXT-2: per-layer step time when P_l layers share one
+        # launch of each kernel, on the small shapes that under-fill the SMs
+        for cfg, kvh in [(configs.high_concurrency(1), None), (configs.high_concurrency(8), None),
+                         (configs.high_concurrency(32), None), (configs.QWEN3_32B, (0, 1))]:
+            for pl in (1, 2, 4, 8):
+                step = DecodeStep(cfg, "cuda", kv_heads=kvh, layers=pl)
+                step.fill_synthetic()
+                t = timed(step.run, args.steps, args.warmup)
+                core = cfg.core_bytes(step.n_kv) * pl
+                lines.append({"workload": cfg.name, "kv_heads_on_gpu": step.n_kv, "layers_packed": pl,
+                              "us_per_launch": t, "us_per_layer": t / pl,
+                              "hbm_tb_per_s": core / (t * 1e-6) / 1e12,
+                              "roofline_frac": core / (t * 1e-6) / 1e9 / _peak()})
+                print(json.dumps(lines[-1]), flush=True)
+                del step
+                torch.cuda.empty_cache()
     else:
         for e in range(0, 10):                                 # batch 1 .. 512
             cfg = configs.high_concurrency(1 << e)

@@ -315,6 +315,41 @@ def test_step_qwen3_32b_graph_sampled_rows_and_determinism():
     torch.cuda.empty_cache()
 
 
+def test_layer_packed_step_bit_identical():
+    """NEXT-2: one launch per kernel over P_l = 3 stacked layers
+    reproduces the three single-layer steps bit for bit, and a packed layer is
+    checked against the oracle on sampled rows."""
+    cfg = configs.QWEN3_8B.with_(batch=3, seq_len=4096, top_k=256)
+    packed = DecodeStep(cfg, DEV, layers=3)
+    packed.fill_synthetic()
+    packed.run()
+    B = cfg.batch
+    for layer in range(3):
+        one = DecodeStep(cfg, DEV)
+        one.fill_synthetic(synth.base_seed(cfg.index) + synth.LAYER_SEED_STRIDE * layer)
+        one.run()
+        torch.cuda.synchronize()
+        rows = slice(layer * B, (layer + 1) * B)
+        assert torch.equal(one.q_hat, packed.q_hat[rows])
+        assert torch.equal(one.sel_idx, packed.sel_idx[rows])
+        assert torch.equal(one.out, packed.out[rows])
+    # layer 2 of the pack against the oracle (chained), batch row 1, KV head 5
+    sd = synth.base_seed(cfg.index) + 2 * synth.LAYER_SEED_STRIDE
+    G, b, h = cfg.group, 1, 5
+    K = synth.kv_rows(sd, synth.STREAM_K, b, h, 0, cfg.seq_len, cfg.n_kv_heads, cfg.seq_len,
+                      cfg.head_dim)[None, None]
+    V = synth.kv_rows(sd, synth.STREAM_V, b, h, 0, cfg.seq_len, cfg.n_kv_heads, cfg.seq_len,
+                      cfg.head_dim)[None, None]
+    r = 2 * B + b
+    qh = packed.q_hat[r:r + 1, h * G:(h + 1) * G].cpu().numpy()
+    s_or, _ = oracle.score(qh, K, [cfg.seq_len])
+    idx = packed.sel_idx[r:r + 1, h:h + 1].cpu().numpy()
+    check_selection(idx[0, 0], s_or[0, 0], cfg.seq_len, cfg.top_k)
+    q = from_dev_bf16(packed.q[r:r + 1, h * G:(h + 1) * G])
+    o_or = oracle.sparse_decode(q, K, V, idx, [cfg.seq_len])
+    assert rel_inf_err(packed.out[r:r + 1, h * G:(h + 1) * G].cpu().numpy(), o_or) <= ATTN_RTOL
+
+
 def test_kv_head_shards_bit_identical():
     """§8(e): P = 2 KV-head shards reproduce the P = 1 slices bit for bit."""
     cfg = configs.QWEN3_8B.with_(batch=4, seq_len=8192, top_k=512)

@@ -47,6 +47,9 @@ def _args():
     ap.add_argument("--emulate-shard", type=int, default=0, metavar="P",
                     help="one GPU runs rank 0's shard of a P-way KV-head split (the per-GPU "
                          "work of the P-GPU run; scaling evidence when only one GPU is at hand)")
+    ap.add_argument("--paged", type=int, default=0, metavar="PAGE_SIZE",
+                    help="run on a paged KV pool (HND pages of PAGE_SIZE tokens, random page "
+                         "placement) through the *_paged entry points (SURVEY §8(f) NEXT-4)")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: skip clocks, e2e and the CPU baseline")
     return ap.parse_args()
@@ -227,8 +230,38 @@ def main():
 
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)
+    pool = None
+    if args.paged:
+        # the same logical cache scattered over a pool (random page placement)
+        k_pool, bt = asp.page_pool(step.k_cache, args.paged, torch.Generator().manual_seed(7))
+        step.k_cache = None
+        torch.cuda.empty_cache()
+        v_pool, _ = asp.page_pool(step.v_cache, args.paged, torch.Generator().manual_seed(7))
+        step.v_cache = None
+        torch.cuda.empty_cache()
+        pool = (k_pool, v_pool, bt)
+        args.no_e2e = args.no_a5 = True
+
+    def one_step_paged(evs=None):
+        k_pool, v_pool, bt = pool
+        if evs is not None:
+            evs[0].record(stream)
+        asp.predict_query(step.window, step.q_hat, dev_flags=step.dev_flags, params=step.p_pred)
+        if evs is not None:
+            evs[1].record(stream)
+        asp.score_select_paged(step.q_hat, k_pool, bt, step.seq_lens, cfg.top_k, cfg.seq_len,
+                               sel_idx=step.sel_idx, workspace=step.ws_sel,
+                               dev_flags=step.dev_flags)
+        if evs is not None:
+            evs[2].record(stream)
+        asp.sparse_decode_paged(step.q, k_pool, v_pool, bt, step.seq_lens, step.sel_idx,
+                                cfg.seq_len, out=step.out, workspace=step.ws_dec)
+        if evs is not None:
+            evs[3].record(stream)
 
     def one_step(evs=None):
+        if pool is not None:
+            return one_step_paged(evs)
         if evs is not None:
             evs[0].record(stream)
         asp.predict_query(step.window, step.q_hat, dev_flags=step.dev_flags, params=step.p_pred)
@@ -419,6 +452,8 @@ def main():
             "config": {"workload": cfg.name, "batch": cfg.batch, "n_q_heads": cfg.n_q_heads,
                        "n_kv_heads": cfg.n_kv_heads, "head_dim": cfg.head_dim,
                        "seq_len": cfg.seq_len, "top_k": cfg.top_k, "window": cfg.window,
+                       "kv_layout": (f"paged: {args.paged}-token HND pages, random placement"
+                                     if args.paged else "dense [B][Hkv][L][D]"),
                        "parallelism": f"kv-head shard x{world}" if shards == world else
                                       f"emulated: rank 0 of a {shards}-way kv-head shard on 1 GPU",
                        "l2": "no flush: K+V per GPU (%.2f GB) >> 126 MB L2" %

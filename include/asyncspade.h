@@ -203,6 +203,49 @@ ASP_API asp_status asyncspade_sparse_decode(const asp_decode_params *p, const as
                                     const int32_t *seq_lens, const int32_t *sel_idx, float *out,
                                     void *workspace, size_t workspace_bytes, asp_stream stream);
 
+/* ------------------------------------------------------------------------
+ * Paged KV caches: the block-table layout of paged
+ * serving engines, which the paper's baselines run on (P:45, P:78,
+ * P:461-465).  The selection itself is unchanged -- token granularity over
+ * the LOGICAL token positions of each sequence -- only where a token's K/V
+ * row lives differs.
+ *
+ * A pool holds `num_pages` pages; a page holds `page_size` consecutive
+ * tokens of every KV head, head-major inside the page (HND):
+ *     element (page, h, t, d) at ((page * n_kv_heads + h) * page_size + t) * head_dim + d
+ * Logical token n of sequence b lives in page
+ *     block_table[b * max_pages_per_seq + n / page_size], slot n % page_size.
+ * page_size is 16, 32, 64 or 128; num_pages * n_kv_heads * page_size < 2^31.
+ * Only the block-table entries of pages a sequence uses (n < seq_lens[b])
+ * are read; an id outside [0, num_pages) is clamped (the result is then
+ * unspecified, but nothing outside the pool is touched).  max_seq_len of the
+ * params must be <= max_pages_per_seq * page_size.  The params' k/v strides
+ * are ignored.  Everything else -- outputs, precision, determinism, error
+ * behaviour -- is that of the dense call: a paged call returns bit for bit
+ * what the dense call returns on the same logical cache.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    int32_t page_size, max_pages_per_seq, num_pages;
+} asp_paged_kv;
+
+/* a2+a3 over a paged K pool (k_pages: device bf16 pool; block_table: device
+ * int32 [batch][max_pages_per_seq]).  Workspace as asyncspade_score_select. */
+ASP_API asp_status asyncspade_score_select_paged(const asp_select_params *p, const asp_paged_kv *pk,
+                                         const float *q_hat, const asp_bf16 *k_pages,
+                                         const int32_t *block_table, const int32_t *seq_lens,
+                                         int32_t *sel_idx, float *scores, void *workspace,
+                                         size_t workspace_bytes, uint32_t *dev_flags,
+                                         asp_stream stream);
+
+/* a4 over paged K and V pools (same geometry and block table for both).
+ * Workspace as asyncspade_sparse_decode. */
+ASP_API asp_status asyncspade_sparse_decode_paged(const asp_decode_params *p, const asp_paged_kv *pk,
+                                          const asp_bf16 *q, const asp_bf16 *k_pages,
+                                          const asp_bf16 *v_pages, const int32_t *block_table,
+                                          const int32_t *seq_lens, const int32_t *sel_idx,
+                                          float *out, void *workspace, size_t workspace_bytes,
+                                          asp_stream stream);
+
 /* Human-readable name of a status code (static storage). */
 ASP_API const char *asyncspade_status_string(asp_status s);
 /* ASYNCSPADE_ABI_VERSION the library was built with. */

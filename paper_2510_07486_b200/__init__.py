@@ -9,6 +9,8 @@ library or a CUDA device is missing, calls raise.
     predict_query   a1  q_hat from the query window           (Alg.1 Steps 1-6)
     score_select    a2+a3  q_hat.K scores + per-row top-k
     sparse_decode   a4  attention over the selected K/V
+    score_select_paged / sparse_decode_paged   the same over a paged KV pool
+                        (block table, HND pages)
 """
 from __future__ import annotations
 
@@ -30,6 +32,7 @@ AGG_MAX, AGG_SUM = 0, 1
 EXPORTED_SYMBOLS = (
     "asyncspade_predict_query", "asyncspade_score_select_workspace", "asyncspade_score_select",
     "asyncspade_sparse_decode_workspace", "asyncspade_sparse_decode",
+    "asyncspade_score_select_paged", "asyncspade_sparse_decode_paged",
     "asyncspade_status_string", "asyncspade_abi_version",
 )
 
@@ -58,6 +61,11 @@ class DecodeParams(ctypes.Structure):
                 ("k_stride_b", ctypes.c_int64), ("k_stride_h", ctypes.c_int64),
                 ("k_stride_t", ctypes.c_int64), ("v_stride_b", ctypes.c_int64),
                 ("v_stride_h", ctypes.c_int64), ("v_stride_t", ctypes.c_int64)]
+
+
+class PagedKV(ctypes.Structure):
+    _fields_ = [("page_size", ctypes.c_int32), ("max_pages_per_seq", ctypes.c_int32),
+                ("num_pages", ctypes.c_int32)]
 
 
 class AsyncSpadeError(RuntimeError):
@@ -92,6 +100,14 @@ def lib() -> ctypes.CDLL:
         L.asyncspade_sparse_decode.argtypes = [ctypes.POINTER(DecodeParams), vp, vp, vp, vp, vp,
                                                vp, vp, sz, vp]
         L.asyncspade_sparse_decode.restype = ctypes.c_int32
+        L.asyncspade_score_select_paged.argtypes = [ctypes.POINTER(SelectParams),
+                                                    ctypes.POINTER(PagedKV), vp, vp, vp, vp, vp,
+                                                    vp, vp, sz, vp, vp]
+        L.asyncspade_score_select_paged.restype = ctypes.c_int32
+        L.asyncspade_sparse_decode_paged.argtypes = [ctypes.POINTER(DecodeParams),
+                                                     ctypes.POINTER(PagedKV), vp, vp, vp, vp, vp,
+                                                     vp, vp, vp, sz, vp]
+        L.asyncspade_sparse_decode_paged.restype = ctypes.c_int32
         L.asyncspade_status_string.argtypes = [ctypes.c_int32]
         L.asyncspade_status_string.restype = ctypes.c_char_p
         L.asyncspade_abi_version.argtypes = []
@@ -226,3 +242,88 @@ def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
                                           _ptr(out), _ptr(workspace), ws_bytes, _stream(stream)),
            "asyncspade_sparse_decode")
     return out
+
+
+# --------------------------------------------------------------------------- paged pools
+def paged_kv(k_pages: torch.Tensor, block_table: torch.Tensor) -> PagedKV:
+    """Geometry of a paged pool k_pages bf16 [num_pages, Hkv, page_size, D]
+    (contiguous, HND) with block_table int32 [batch, max_pages_per_seq]."""
+    n_pages, _, P, _ = k_pages.shape
+    if not k_pages.is_contiguous() or not block_table.is_contiguous():
+        raise AsyncSpadeError("the page pool and block table must be contiguous")
+    return PagedKV(P, block_table.shape[1], n_pages)
+
+
+def score_select_paged(q_hat: torch.Tensor, k_pages: torch.Tensor, block_table: torch.Tensor,
+                       seq_lens: torch.Tensor, top_k: int, max_seq_len: int, *,
+                       sel_idx: torch.Tensor | None = None, scores: torch.Tensor | None = None,
+                       workspace: torch.Tensor | None = None, aggregation: int = AGG_MAX,
+                       dev_flags: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """a2+a3 over a paged K pool -> asyncspade_score_select_paged.  Returns
+    sel_idx int32 [B, Hkv, top_k] of LOGICAL token positions."""
+    B, Hq, D = q_hat.shape
+    Hkv = k_pages.shape[1]
+    p = SelectParams(B, Hq, Hkv, D, top_k, max_seq_len, aggregation, 0, 0, D)
+    pk = paged_kv(k_pages, block_table)
+    if sel_idx is None:
+        sel_idx = torch.empty(B, Hkv, top_k, dtype=torch.int32, device=q_hat.device)
+    ws_bytes = 0
+    if scores is None:
+        ws_bytes = score_select_workspace(p)
+        if workspace is None:
+            workspace = _workspace(ws_bytes, q_hat.device)
+        ws_bytes = workspace.numel() * workspace.element_size()
+    _check(lib().asyncspade_score_select_paged(ctypes.byref(p), ctypes.byref(pk), _ptr(q_hat),
+                                               _ptr(_u16(k_pages)), _ptr(block_table),
+                                               _ptr(seq_lens), _ptr(sel_idx), _ptr(scores),
+                                               _ptr(workspace), ws_bytes, _ptr(dev_flags),
+                                               _stream(stream)),
+           "asyncspade_score_select_paged")
+    return sel_idx
+
+
+def sparse_decode_paged(q: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor,
+                        block_table: torch.Tensor, seq_lens: torch.Tensor, sel_idx: torch.Tensor,
+                        max_seq_len: int, *, n_fresh: int = 0, sm_scale: float | None = None,
+                        out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+                        stream=None) -> torch.Tensor:
+    """a4 over paged K / V pools -> asyncspade_sparse_decode_paged."""
+    B, Hq, D = q.shape
+    Hkv = k_pages.shape[1]
+    if sm_scale is None:
+        sm_scale = D ** -0.5
+    p = DecodeParams(B, Hq, Hkv, D, sel_idx.shape[-1], n_fresh, max_seq_len, sm_scale,
+                     0, 0, D, 0, 0, D)
+    pk = paged_kv(k_pages, block_table)
+    if out is None:
+        out = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+    if workspace is None:
+        workspace = _workspace(sparse_decode_workspace(p), q.device)
+    ws_bytes = workspace.numel() * workspace.element_size()
+    _check(lib().asyncspade_sparse_decode_paged(ctypes.byref(p), ctypes.byref(pk), _ptr(_u16(q)),
+                                                _ptr(_u16(k_pages)), _ptr(_u16(v_pages)),
+                                                _ptr(block_table), _ptr(seq_lens), _ptr(sel_idx),
+                                                _ptr(out), _ptr(workspace), ws_bytes,
+                                                _stream(stream)),
+           "asyncspade_sparse_decode_paged")
+    return out
+
+
+def page_pool(cache: torch.Tensor, page_size: int, generator: torch.Generator | None = None,
+              spare_pages: int = 0):
+    """Scatter a dense cache [B, Hkv, L, D] into a paged pool with a random
+    page placement: returns (pool [B*L/P + spare, Hkv, P, D], block_table
+    int32 [B, L/P]).  Data movement only (torch ops); used to build paged
+    inputs for tests and the bench, not on the path."""
+    B, Hkv, L, D = cache.shape
+    if L % page_size:
+        raise AsyncSpadeError("L must be a multiple of page_size")
+    npp = L // page_size
+    n_pages = B * npp + spare_pages
+    perm = torch.randperm(n_pages, generator=generator)[:B * npp].to(torch.int32)
+    block_table = perm.view(B, npp).to(cache.device)
+    pool = torch.zeros(n_pages, Hkv, page_size, D, dtype=cache.dtype, device=cache.device)
+    src = cache.view(B, Hkv, npp, page_size, D).permute(0, 2, 1, 3, 4).reshape(B * npp, Hkv,
+                                                                                 page_size, D)
+    pool[block_table.view(-1).long()] = src
+    return pool, block_table

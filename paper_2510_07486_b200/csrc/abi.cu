@@ -50,6 +50,16 @@ asp_status check_decode(const asp_decode_params *p) {
     return ASP_OK;
 }
 
+asp_status check_paged(const asp_paged_kv *pk, int n_kv_heads, int max_seq_len) {
+    if (!pk) return ASP_ERR_INVALID_ARGUMENT;
+    const int P = pk->page_size;
+    if (P != 16 && P != 32 && P != 64 && P != 128) return ASP_ERR_UNSUPPORTED;
+    if (pk->max_pages_per_seq <= 0 || pk->num_pages <= 0) return ASP_ERR_SHAPE;
+    if ((int64_t)pk->max_pages_per_seq * P < max_seq_len) return ASP_ERR_SHAPE;
+    if ((int64_t)pk->num_pages * n_kv_heads * P >= ((int64_t)1 << 31)) return ASP_ERR_SHAPE;
+    return ASP_OK;
+}
+
 }  // namespace
 
 int asp_sm_count() {
@@ -111,6 +121,35 @@ asp_status asyncspade_score_select(const asp_select_params *p, const float *q_ha
     return from_cuda(asp_launch_select(*p, s_buf, seq_lens, sel_idx, dev_flags, scores == nullptr, s));
 }
 
+asp_status asyncspade_score_select_paged(const asp_select_params *p, const asp_paged_kv *pk,
+                                         const float *q_hat, const asp_bf16 *k_pages,
+                                         const int32_t *block_table, const int32_t *seq_lens,
+                                         int32_t *sel_idx, float *scores, void *workspace,
+                                         size_t workspace_bytes, uint32_t *dev_flags,
+                                         asp_stream stream) {
+    if (!p) return ASP_ERR_INVALID_ARGUMENT;
+    asp_select_params q = *p;                        // strides are the pool's (ignored)
+    q.k_stride_t = q.head_dim;
+    q.k_stride_h = q.k_stride_b = 0;
+    asp_status st = check_select(&q);
+    if (st != ASP_OK) return st;
+    st = check_paged(pk, q.n_kv_heads, q.max_seq_len);
+    if (st != ASP_OK) return st;
+    if (!q_hat || !k_pages || !block_table || !seq_lens || !sel_idx) return ASP_ERR_INVALID_ARGUMENT;
+    if (!aligned16(q_hat) || !aligned16(k_pages) || !aligned16(scores)) return ASP_ERR_INVALID_ARGUMENT;
+    float *s_buf = scores;
+    if (!s_buf) {
+        if (!workspace || workspace_bytes < asyncspade_score_select_workspace(&q))
+            return ASP_ERR_WORKSPACE;
+        if (reinterpret_cast<uintptr_t>(workspace) & 255u) return ASP_ERR_WORKSPACE;
+        s_buf = static_cast<float *>(workspace);
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = asp_launch_score(q, q_hat, k_pages, seq_lens, s_buf, dev_flags, s, pk, block_table);
+    if (e != cudaSuccess) return ASP_ERR_CUDA;
+    return from_cuda(asp_launch_select(q, s_buf, seq_lens, sel_idx, dev_flags, scores == nullptr, s));
+}
+
 size_t asyncspade_sparse_decode_workspace(const asp_decode_params *p) {
     if (check_decode(p) != ASP_OK) return 0;
     return align256(asp_decode_partials_bytes(*p));
@@ -129,6 +168,31 @@ asp_status asyncspade_sparse_decode(const asp_decode_params *p, const asp_bf16 *
     if (reinterpret_cast<uintptr_t>(workspace) & 255u) return ASP_ERR_WORKSPACE;
     return from_cuda(asp_launch_decode(*p, q, k_cache, v_cache, seq_lens, sel_idx, out,
                                        static_cast<float *>(workspace), (cudaStream_t)stream));
+}
+
+asp_status asyncspade_sparse_decode_paged(const asp_decode_params *p, const asp_paged_kv *pk,
+                                          const asp_bf16 *q, const asp_bf16 *k_pages,
+                                          const asp_bf16 *v_pages, const int32_t *block_table,
+                                          const int32_t *seq_lens, const int32_t *sel_idx,
+                                          float *out, void *workspace, size_t workspace_bytes,
+                                          asp_stream stream) {
+    if (!p) return ASP_ERR_INVALID_ARGUMENT;
+    asp_decode_params d = *p;                        // strides are the pool's (ignored)
+    d.k_stride_t = d.v_stride_t = d.head_dim;
+    d.k_stride_h = d.k_stride_b = d.v_stride_h = d.v_stride_b = 0;
+    asp_status st = check_decode(&d);
+    if (st != ASP_OK) return st;
+    st = check_paged(pk, d.n_kv_heads, d.max_seq_len);
+    if (st != ASP_OK) return st;
+    if (!q || !k_pages || !v_pages || !block_table || !seq_lens || !sel_idx || !out)
+        return ASP_ERR_INVALID_ARGUMENT;
+    if (!aligned16(q) || !aligned16(k_pages) || !aligned16(v_pages) || !aligned16(out))
+        return ASP_ERR_INVALID_ARGUMENT;
+    if (!workspace || workspace_bytes < asyncspade_sparse_decode_workspace(&d)) return ASP_ERR_WORKSPACE;
+    if (reinterpret_cast<uintptr_t>(workspace) & 255u) return ASP_ERR_WORKSPACE;
+    return from_cuda(asp_launch_decode(d, q, k_pages, v_pages, seq_lens, sel_idx, out,
+                                       static_cast<float *>(workspace), (cudaStream_t)stream, pk,
+                                       block_table));
 }
 
 const char *asyncspade_status_string(asp_status s) {

@@ -93,9 +93,11 @@ cudaError_t asp_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 // host-side validation).  They return cudaGetLastError() of the launch.
 cudaError_t asp_launch_predict(const asp_predict_params &p, const float *q_window, float *q_hat,
                                uint32_t *dev_flags, cudaStream_t s);
+// pk / block_table: a paged pool (asyncspade_*_paged), or nullptr (dense cache)
 cudaError_t asp_launch_score(const asp_select_params &p, const float *q_hat,
                              const asp_bf16 *k_cache, const int32_t *seq_lens, float *scores,
-                             uint32_t *dev_flags, cudaStream_t s);
+                             uint32_t *dev_flags, cudaStream_t s,
+                             const asp_paged_kv *pk = nullptr, const int32_t *block_table = nullptr);
 // discard_scores: the scores live in the caller's workspace and are dead
 // after selection -- their L2 lines are dropped without write-back.
 cudaError_t asp_launch_select(const asp_select_params &p, const float *scores,
@@ -105,5 +107,6 @@ size_t asp_decode_partials_bytes(const asp_decode_params &p);
 cudaError_t asp_launch_decode(const asp_decode_params &p, const asp_bf16 *q,
                               const asp_bf16 *k_cache, const asp_bf16 *v_cache,
                               const int32_t *seq_lens, const int32_t *sel_idx, float *out,
-                              float *partials, cudaStream_t s);
+                              float *partials, cudaStream_t s,
+                              const asp_paged_kv *pk = nullptr, const int32_t *block_table = nullptr);
 int asp_sm_count();

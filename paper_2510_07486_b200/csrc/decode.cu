@@ -81,12 +81,18 @@ struct Item {
     int row, chunk;
 };
 
-template <int D, int G>
+// Paged pools (asyncspade_sparse_decode_paged); unused by the dense instantiation.
+struct PagedArgs {
+    const int32_t *block_table;
+    int page_size, max_pages, num_pages;
+};
+
+template <int D, int G, bool PAGED>
 __global__ void __launch_bounds__(kThreads, 1)
 decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                  const asp_bf16 *__restrict__ k_cache, const asp_bf16 *__restrict__ v_cache,
                  const int32_t *__restrict__ seq_lens, const int32_t *__restrict__ sel_idx,
-                 float *__restrict__ partials, int n_splits) {
+                 float *__restrict__ partials, int n_splits, PagedArgs pg) {
     using C = DCfg<D>;
     extern __shared__ unsigned char smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -186,7 +192,45 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                 pre_raw[u] = e < p.top_k ? __ldg(ib + e) : -1;
             }
         };
+        // the attended token of entry u of item `it` (-1: none): a selected index
+        // below the fresh tail, or a fresh-tail position (reading R12)
+        auto logical_tok = [&](const Item &it, int len, int raw_u, int u) {
+            const int fresh_lo = max(len - p.n_fresh, 0);
+            const int e = it.chunk * kChunk + pt + u * kProducerThreads;
+            int tok = -1;
+            if (e < p.top_k) {
+                if (raw_u >= 0 && raw_u < fresh_lo) tok = raw_u;
+            } else if (e < E) {
+                const int t = fresh_lo + (e - p.top_k);
+                if (t < len) tok = t;
+            }
+            return tok;
+        };
+        // Paged pools: s_tok holds the token's POOL row, (page * Hkv + h) *
+        // page_size + slot.  The block-table lookups of item i+1 are issued
+        // while item i is prepared (indices fetched two items ahead), so the
+        // dependent loads never stall the gather.
+        int x_tok[kEntriesPerThread] = {};
+        auto xlate = [&](int i) {                             // uses pre_* of item i
+            const Item it = item(i);
+            const int b = it.row / Hkv, h = it.row % Hkv;
+            const int len = min(max(pre_len, 0), p.max_seq_len);
+#pragma unroll
+            for (int u = 0; u < kEntriesPerThread; u++) {
+                const int tok = logical_tok(it, len, pre_raw[u], u);
+                int id = 0;
+                if (tok >= 0) {
+                    id = __ldg(pg.block_table + (size_t)b * pg.max_pages + tok / pg.page_size);
+                    id = min(max(id, 0), pg.num_pages - 1);   // never fault on a bad entry
+                }
+                x_tok[u] = tok < 0 ? -1 : (id * Hkv + h) * pg.page_size + tok % pg.page_size;
+            }
+        };
         if (n_items > 0) fetch(0);
+        if (PAGED && n_items > 0) {
+            xlate(0);
+            if (n_items > 1) fetch(1);
+        }
         constexpr int kLag = 2;                               // < kStages
         int pending[kLag + 1];
         int npend = 0;
@@ -219,31 +263,28 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                 }
                 fence_proxy_async_smem();
             }
-            // this item's indices were fetched one item ahead (pre_*); fetch the next
-            const int len = min(max(pre_len, 0), p.max_seq_len);
-            int raw[kEntriesPerThread];
+            int toks[kEntriesPerThread];
+            if (PAGED) {
+                // this item's pool rows were resolved one item ahead (x_tok);
+                // resolve the next one and fetch the indices of the one after
 #pragma unroll
-            for (int u = 0; u < kEntriesPerThread; u++) raw[u] = pre_raw[u];
-            if (i + 1 < n_items) fetch(i + 1);
+                for (int u = 0; u < kEntriesPerThread; u++) toks[u] = x_tok[u];
+                if (i + 1 < n_items) xlate(i + 1);
+                if (i + 2 < n_items) fetch(i + 2);
+            } else {
+                // this item's indices were fetched one item ahead (pre_*); fetch the next
+                const int len = min(max(pre_len, 0), p.max_seq_len);
+#pragma unroll
+                for (int u = 0; u < kEntriesPerThread; u++) toks[u] = logical_tok(it, len, pre_raw[u], u);
+                if (i + 1 < n_items) fetch(i + 1);
+            }
             DWAIT(1, mbar_wait(bar(B_TOKEMPTY + slot), ((i >> 1) & 1) ^ 1));
             // WAR: every producer thread must be done reading this slot for the
             // previous item's V gather before anyone overwrites it
             asm volatile("bar.sync 2, %0;" ::"n"(kProducerThreads) : "memory");
-            const int fresh_lo = max(len - p.n_fresh, 0);
 #pragma unroll
-            for (int u = 0; u < kEntriesPerThread; u++) {
-                const int j = pt + u * kProducerThreads;
-                const int e = it.chunk * kChunk + j;
-                int tok = -1;
-                if (e < p.top_k) {
-                    const int t = raw[u];
-                    if (t >= 0 && t < fresh_lo) tok = t;
-                } else if (e < E) {
-                    const int t = fresh_lo + (e - p.top_k);
-                    if (t < len) tok = t;
-                }
-                s_tok[slot * kChunk + j] = tok;
-            }
+            for (int u = 0; u < kEntriesPerThread; u++)
+                s_tok[slot * kChunk + pt + u * kProducerThreads] = toks[u];
             asm volatile("bar.sync 2, %0;" ::"n"(kProducerThreads) : "memory");
             if (pt == 0) {
                 mbar_arrive(bar(B_TOKFULL + slot));
@@ -254,7 +295,8 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             const int slot = i & 1;
             const Item it = item(i);
             const int b = it.row / Hkv, h = it.row % Hkv;
-            const asp_bf16 *rowbase = cache + b * sb + h * sh;
+            const asp_bf16 *rowbase = PAGED ? cache : cache + b * sb + h * sh;
+            if (PAGED) st = D;                                // pool rows
             constexpr int kChunksPerRow = D / 8;              // 16-B chunks per token row
             constexpr int kRowsPerPass = kProducerThreads / kChunksPerRow;
             const int chunk = pt % kChunksPerRow;
@@ -552,16 +594,20 @@ int n_splits_of(const asp_decode_params &p) {
 template <int D, int G>
 cudaError_t launch(const asp_decode_params &p, const asp_bf16 *q, const asp_bf16 *k,
                    const asp_bf16 *v, const int32_t *seq_lens, const int32_t *idx, float *out,
-                   float *partials, cudaStream_t s) {
+                   float *partials, cudaStream_t s, const asp_paged_kv *pk,
+                   const int32_t *block_table) {
     using C = DCfg<D>;
     const int ns = n_splits_of(p);
     const long total = (long)p.batch * p.n_kv_heads * ns;
     const int grid = (int)(total < asp_sm_count() ? total : asp_sm_count());
-    cudaError_t e = cudaFuncSetAttribute(decode_tc_kernel<D, G>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    PagedArgs pg{block_table, pk ? pk->page_size : 1, pk ? pk->max_pages_per_seq : 0,
+                 pk ? pk->num_pages : 0};
+    auto kern = pk ? decode_tc_kernel<D, G, true> : decode_tc_kernel<D, G, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::kSmemBytes);
     if (e != cudaSuccess) return e;
-    e = asp_launch(decode_tc_kernel<D, G>, dim3(grid), dim3(kThreads), C::kSmemBytes, s, 1, p, q,
-                   k, v, seq_lens, idx, partials, ns);
+    e = asp_launch(kern, dim3(grid), dim3(kThreads), C::kSmemBytes, s, 1, p, q, k, v, seq_lens,
+                   idx, partials, ns, pg);
     if (e != cudaSuccess) return e;
     return asp_launch(decode_combine_kernel<D>, dim3(p.n_q_heads, p.batch), dim3(D), 0, s, 1, p,
                       (const float *)partials, out, ns);
@@ -585,11 +631,12 @@ size_t asp_decode_partials_bytes(const asp_decode_params &p) {
 cudaError_t asp_launch_decode(const asp_decode_params &p, const asp_bf16 *q,
                               const asp_bf16 *k_cache, const asp_bf16 *v_cache,
                               const int32_t *seq_lens, const int32_t *sel_idx, float *out,
-                              float *partials, cudaStream_t s) {
+                              float *partials, cudaStream_t s, const asp_paged_kv *pk,
+                              const int32_t *block_table) {
     const int G = p.n_q_heads / p.n_kv_heads;
 #define ASP_CASE(DD, GG) \
     if (p.head_dim == DD && G == GG) \
-        return launch<DD, GG>(p, q, k_cache, v_cache, seq_lens, sel_idx, out, partials, s);
+        return launch<DD, GG>(p, q, k_cache, v_cache, seq_lens, sel_idx, out, partials, s, pk, block_table);
     ASP_CASE(64, 1) ASP_CASE(64, 2) ASP_CASE(64, 4) ASP_CASE(64, 8)
     ASP_CASE(128, 1) ASP_CASE(128, 2) ASP_CASE(128, 4) ASP_CASE(128, 8)
 #undef ASP_CASE

@@ -211,11 +211,19 @@ struct TileIter {
     }
 };
 
-template <int D, int G>
+// Paged pool (asyncspade_score_select_paged): the block table and the pool
+// geometry; unused by the dense instantiation.
+struct PagedArgs {
+    const int32_t *block_table;
+    int page_size, max_pages, num_pages;
+};
+
+template <int D, int G, bool PAGED>
 __global__ void __launch_bounds__(kThreads, 1)
 score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
                 const float *__restrict__ q_hat, const int32_t *__restrict__ seq_lens,
-                float *__restrict__ scores, uint32_t *dev_flags, int tiles_per_row) {
+                float *__restrict__ scores, uint32_t *dev_flags, int tiles_per_row,
+                PagedArgs pg) {
     using C = Cfg<D, G>;
     constexpr int N = C::N;
     extern __shared__ unsigned char smem_raw[];
@@ -264,7 +272,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
     const long long t_kernel0 = clock64();
 #endif
 
-    if (warp == 0) {
+    if (warp == 0 && !PAGED) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
             int s = 0;
@@ -285,6 +293,56 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
                 if (++s == kStages) { s = 0; ph ^= 1; }
             }
             PFLUSH(0, pw_empty);
+        }
+        __syncwarp();
+    } else if (warp == 0) {
+        // ------------------------------------------------ TMA producer, paged pool
+        // A 128-token tile is NP = 128 / page_size pages; each page is a
+        // [page_size][D] box of the pool's [rows][D] view (row = (page * Hkv +
+        // h) * page_size + t), landing at its token offset in the stage (the
+        // 128-B swizzle repeats every 8 rows, so the boxes compose).  The whole
+        // warp walks the tile sequence: lanes < NP fetch the page ids of the
+        // tile kAhead positions ahead (one block-table word each), so the
+        // lookups never stall the stream, and issue that page's copies.
+        constexpr int kAhead = 3;
+        const int P = pg.page_size, NP = kTileM / pg.page_size;
+        TileIter ahead = it;
+        long ia = ahead.next(it.start);
+        auto fetch = [&]() -> int {
+            int id = 0;
+            if (ia < it.end) {
+                const int row = ahead.row, b = row / p.n_kv_heads;
+                const int lp = ahead.j * NP + lane;
+                if (lane < NP && lp * P < ahead.len_of(row)) {
+                    id = __ldg(pg.block_table + (size_t)b * pg.max_pages + lp);
+                    id = min(max(id, 0), pg.num_pages - 1);     // never fault on a bad entry
+                }
+                ia = ahead.next(ia + 1);
+            }
+            return id;
+        };
+        int q0 = fetch(), q1 = fetch(), q2 = fetch();
+        static_assert(kAhead == 3, "the page-id queue is q0..q2");
+        int s = 0;
+        uint32_t ph = 0;
+        for (long i = it.next(it.start); i < it.end; i = it.next(i + 1)) {
+            const int cur = q0;
+            q0 = q1;
+            q1 = q2;
+            q2 = fetch();
+            const int h = it.row % p.n_kv_heads;
+            mbar_wait(empty_bar(s), ph ^ 1);
+            if (lane == 0) mbar_arrive_expect_tx(full_bar(s), C::kStageBytes);
+            __syncwarp();
+            // lane l < NP copies its own page (issue spread over the lanes)
+            const uint32_t dst = stage0 + s * C::kStageBytes;
+            if (lane < NP) {
+#pragma unroll
+                for (int r = 0; r < C::kRegions; r++)
+                    tma_load_2d(dst + r * (kTileM * 128) + lane * P * 128, &kmap, full_bar(s),
+                                r * 64, (cur * p.n_kv_heads + h) * P, kEvictFirst);
+            }
+            if (++s == kStages) { s = 0; ph ^= 1; }
         }
         __syncwarp();
     } else if (warp == 1) {
@@ -493,18 +551,24 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 template <int D, int G>
 cudaError_t launch(const asp_select_params &p, const float *q_hat, const asp_bf16 *k,
-                   const int32_t *seq_lens, float *scores, uint32_t *dev_flags, cudaStream_t s) {
+                   const int32_t *seq_lens, float *scores, uint32_t *dev_flags, cudaStream_t s,
+                   const asp_paged_kv *pk, const int32_t *block_table) {
     using C = Cfg<D, G>;
     auto encode = get_encode();
     if (!encode) return cudaErrorNotSupported;
-    // 2-D row view [rows][D] of the cache: row(b, h, t) = (b*sb + h*sh)/st + t
-    // (the ABI requires sb, sh to be multiples of st); a tile is 128 rows.
+    // 2-D row view [rows][D]: dense cache row(b, h, t) = (b*sb + h*sh)/st + t
+    // (the ABI requires sb, sh to be multiples of st), a tile is one 128-row
+    // box; paged pool row(page, h, t) = (page * Hkv + h) * page_size + t, a
+    // tile is 128 / page_size boxes of page_size rows.
     CUtensorMap map;
-    const int64_t rows = ((int64_t)(p.batch - 1) * p.k_stride_b +
-                          (int64_t)(p.n_kv_heads - 1) * p.k_stride_h) / p.k_stride_t + p.max_seq_len;
+    const bool paged = pk != nullptr;
+    const int64_t rows = paged ? (int64_t)pk->num_pages * p.n_kv_heads * pk->page_size
+                               : ((int64_t)(p.batch - 1) * p.k_stride_b +
+                                  (int64_t)(p.n_kv_heads - 1) * p.k_stride_h) / p.k_stride_t +
+                                     p.max_seq_len;
     const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
-    const cuuint64_t strides[1] = {(cuuint64_t)p.k_stride_t * 2};
-    const cuuint32_t box[2] = {64, (cuuint32_t)kTileM};
+    const cuuint64_t strides[1] = {(cuuint64_t)(paged ? D : p.k_stride_t) * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)(paged ? pk->page_size : kTileM)};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<asp_bf16 *>(k), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -514,11 +578,14 @@ cudaError_t launch(const asp_select_params &p, const float *q_hat, const asp_bf1
     const int tpr = (p.max_seq_len + kTileM - 1) / kTileM;
     const long total = (long)p.batch * p.n_kv_heads * tpr;
     const int grid = (int)(total < asp_sm_count() ? total : asp_sm_count());
-    cudaError_t e = cudaFuncSetAttribute(score_tc_kernel<D, G>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    PagedArgs pg{block_table, paged ? pk->page_size : 0, paged ? pk->max_pages_per_seq : 0,
+                 paged ? pk->num_pages : 0};
+    auto kern = paged ? score_tc_kernel<D, G, true> : score_tc_kernel<D, G, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::kSmemBytes);
     if (e != cudaSuccess) return e;
-    return asp_launch(score_tc_kernel<D, G>, dim3(grid), dim3(kThreads), C::kSmemBytes, s, 1, map,
-                      p, q_hat, seq_lens, scores, dev_flags, tpr);
+    return asp_launch(kern, dim3(grid), dim3(kThreads), C::kSmemBytes, s, 1, map, p, q_hat,
+                      seq_lens, scores, dev_flags, tpr, pg);
 }
 
 }  // namespace
@@ -534,10 +601,12 @@ extern "C" __attribute__((visibility("default"))) int asp_score_prof_read(unsign
 
 cudaError_t asp_launch_score(const asp_select_params &p, const float *q_hat,
                              const asp_bf16 *k_cache, const int32_t *seq_lens, float *scores,
-                             uint32_t *dev_flags, cudaStream_t s) {
+                             uint32_t *dev_flags, cudaStream_t s, const asp_paged_kv *pk,
+                             const int32_t *block_table) {
     const int G = p.n_q_heads / p.n_kv_heads;
 #define ASP_CASE(DD, GG) \
-    if (p.head_dim == DD && G == GG) return launch<DD, GG>(p, q_hat, k_cache, seq_lens, scores, dev_flags, s);
+    if (p.head_dim == DD && G == GG) \
+        return launch<DD, GG>(p, q_hat, k_cache, seq_lens, scores, dev_flags, s, pk, block_table);
     ASP_CASE(64, 1) ASP_CASE(64, 2) ASP_CASE(64, 4) ASP_CASE(64, 8)
     ASP_CASE(128, 1) ASP_CASE(128, 2) ASP_CASE(128, 4) ASP_CASE(128, 8)
 #undef ASP_CASE

@@ -132,3 +132,30 @@ def test_synth_library_exports():
     from paper_2510_07486_b200 import synth
     L = synth._dev_lib()
     assert hasattr(L, "asp_synth_kv") and hasattr(L, "asp_synth_query")
+
+
+def test_paged_validation(L):
+    """Paged entry points: page sizes 16..128 only, the block table must cover
+    max_seq_len, the pool must stay below 2^31 rows, null pointers rejected."""
+    sp = asp.SelectParams(2, 16, 8, 128, 64, 1024, 0, 0, 0, 128)
+    dp = asp.DecodeParams(2, 16, 8, 128, 64, 0, 1024, 0.088, 0, 0, 128, 0, 0, 128)
+
+    def sel(pk, bt=FAKE):
+        return L.asyncspade_score_select_paged(ctypes.byref(sp), ctypes.byref(pk), FAKE, FAKE, bt,
+                                               FAKE, FAKE, FAKE, None, 0, None, None)
+
+    def dec(pk, bt=FAKE):
+        return L.asyncspade_sparse_decode_paged(ctypes.byref(dp), ctypes.byref(pk), FAKE, FAKE,
+                                                FAKE, bt, FAKE, FAKE, FAKE, None, 0, None)
+
+    for fn in (sel, dec):
+        assert fn(asp.PagedKV(8, 128, 256)) == 3                 # page size not built
+        assert fn(asp.PagedKV(24, 64, 256)) == 3
+        assert fn(asp.PagedKV(16, 32, 256)) == 2                 # 32 * 16 < max_seq_len
+        assert fn(asp.PagedKV(16, 64, 0)) == 2
+        assert fn(asp.PagedKV(128, 8, 1 << 22)) == 2             # pool rows >= 2^31
+        assert fn(asp.PagedKV(16, 64, 256), bt=None) == 1
+    assert L.asyncspade_score_select_paged(ctypes.byref(sp), None, FAKE, FAKE, FAKE, FAKE, FAKE,
+                                           FAKE, None, 0, None, None) == 1
+    # decode needs its workspace: a valid call shape without one is rejected as such
+    assert dec(asp.PagedKV(16, 64, 256)) == 4

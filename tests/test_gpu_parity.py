@@ -473,3 +473,49 @@ def test_async_pipeline_matches_serial():
         assert torch.equal(o_s[t], o_a[t]), t
     # the selections really changed as the window and cache moved
     assert not torch.equal(i_a[0], i_a[T - 1])
+
+
+# ----------------------------------------------------------------------------- paged pools (NEXT-4)
+@pytest.mark.parametrize("G,D,P", [(8, 128, 16), (1, 64, 64), (4, 128, 32), (2, 64, 128)])
+def test_paged_matches_dense_bit_for_bit(G, D, P):
+    """The paged entry points return bit for bit what the dense ones return on
+    the same logical cache (random page placement, spare pages, ragged
+    lengths incl. a row shorter than k and a partial last page, n_fresh = 1),
+    and a paged row passes the oracle (chained)."""
+    B, Hkv, L, k = 4, 2, 1024, 96
+    seed = synth.base_seed(0) + 77 + P
+    K = synth.kv_cache(seed, synth.STREAM_K, B, Hkv, L, D)
+    V = synth.kv_cache(seed, synth.STREAM_V, B, Hkv, L, D)
+    Kd, Vd = to_dev_bf16(K), to_dev_bf16(V)
+    lens = [L, 517, 40, 1000]
+    sl = torch.tensor(lens, dtype=torch.int32, device=DEV)
+    rng = np.random.default_rng(seed)
+    qh = torch.from_numpy((rng.standard_normal((B, Hkv * G, D)) * 0.7).astype(np.float32)).to(DEV)
+    q = torch.from_numpy(rng.standard_normal((B, Hkv * G, D)).astype(np.float32)).to(DEV).to(torch.bfloat16)
+    gen = torch.Generator().manual_seed(seed)
+    k_pool, bt = asp.page_pool(Kd, P, gen, spare_pages=5)
+    gen = torch.Generator().manual_seed(seed)
+    v_pool, bt_v = asp.page_pool(Vd, P, gen, spare_pages=5)
+    assert torch.equal(bt, bt_v)
+    bt = bt.contiguous()
+    s_d = torch.full((B, Hkv, L), np.nan, dtype=torch.float32, device=DEV)
+    s_p = torch.full((B, Hkv, L), np.nan, dtype=torch.float32, device=DEV)
+    idx_d = asp.score_select(qh, Kd, sl, k, scores=s_d)
+    idx_p = asp.score_select_paged(qh, k_pool, bt, sl, k, L, scores=s_p)
+    idx_w = asp.score_select_paged(qh, k_pool, bt, sl, k, L)          # workspace path
+    torch.cuda.synchronize()
+    assert torch.equal(idx_d, idx_p) and torch.equal(idx_p, idx_w)
+    for b in range(B):
+        assert torch.equal(s_d[b, :, :lens[b]], s_p[b, :, :lens[b]])
+    out_d = asp.sparse_decode(q, Kd, Vd, sl, idx_d, n_fresh=1)
+    out_p = asp.sparse_decode_paged(q, k_pool, v_pool, bt, sl, idx_p, L, n_fresh=1)
+    torch.cuda.synchronize()
+    assert torch.equal(out_d, out_p)
+    # oracle, chained, on the ragged row b = 1
+    b = 1
+    so, _ = oracle.score(qh[b:b + 1].cpu().numpy(), K[b:b + 1], [lens[b]])
+    for h in range(Hkv):
+        check_selection(idx_p[b, h].cpu().numpy(), so[0, h], lens[b], k)
+    o_or = oracle.sparse_decode(from_dev_bf16(q[b:b + 1]), K[b:b + 1], V[b:b + 1],
+                                idx_p[b:b + 1].cpu().numpy(), [lens[b]], n_fresh=1)
+    assert rel_inf_err(out_p[b:b + 1].cpu().numpy(), o_or) <= ATTN_RTOL

@@ -47,6 +47,9 @@ def _args():
     ap.add_argument("--emulate-shard", type=int, default=0, metavar="P",
                     help="one GPU runs rank 0's shard of a P-way KV-head split (the per-GPU "
                          "work of the P-GPU run; scaling evidence when only one GPU is at hand)")
+    ap.add_argument("--ragged", action="store_true",
+                    help="ragged batch: seq_lens seeded-uniform in [L/8, L] (the cache capacity "
+                         "stays L; headline bytes count each row's own length)")
     ap.add_argument("--paged", type=int, default=0, metavar="PAGE_SIZE",
                     help="run on a paged KV pool (HND pages of PAGE_SIZE tokens, random page "
                          "placement) through the *_paged entry points (SURVEY §8(f) NEXT-4)")
@@ -211,6 +214,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2510_07486_b200 as asp
+    from paper_2510_07486_b200 import synth
     from paper_2510_07486_b200.step import DecodeStep
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -226,6 +230,12 @@ def main():
     h0, hn = kv_head_shard(cfg.n_kv_heads, shards, rank)    # §8(e): KV-head sharding
     step = DecodeStep(cfg, "cuda", kv_heads=(h0, hn))
     step.fill_synthetic()
+    lens = [cfg.seq_len] * cfg.batch
+    if args.ragged:
+        import numpy as np
+        rng = np.random.default_rng(synth.base_seed(cfg.index) + 99)
+        lens = [int(x) for x in rng.integers(cfg.seq_len // 8, cfg.seq_len + 1, cfg.batch)]
+        step.seq_lens.copy_(torch.tensor(lens, dtype=torch.int32))
     torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
@@ -415,6 +425,7 @@ def main():
         torch.cuda.empty_cache()
         st1 = DecodeStep(cfg, "cuda", kv_heads=(h0, hn), n_fresh=1)
         st1.fill_synthetic()
+        st1.seq_lens.copy_(torch.tensor(lens, dtype=torch.int32))
         pipe = AsyncPipeline(st1)
         res = {}
         for name, fn in (("serial", pipe.run_step_serial), ("pipelined", pipe.run_step)):
@@ -441,8 +452,9 @@ def main():
 
     if rank == 0:
         peak, peak_src = _peaks()
-        core = cfg.core_bytes(hn)                      # per GPU
-        k_bytes = cfg.batch * hn * cfg.seq_len * cfg.head_dim * 2
+        D2 = cfg.head_dim * 2                          # per GPU: full-K + selected K and V
+        k_bytes = sum(lens) * hn * D2
+        core = k_bytes + 2 * sum(min(cfg.top_k, n) for n in lens) * hn * D2
         achieved = k_bytes / (avg_sel_max * 1e-3) / 1e9
         line = {
             "metric": METRIC, "value": ms_step * 1e3, "unit": UNIT, "n_gpus": world,
@@ -452,6 +464,8 @@ def main():
             "config": {"workload": cfg.name, "batch": cfg.batch, "n_q_heads": cfg.n_q_heads,
                        "n_kv_heads": cfg.n_kv_heads, "head_dim": cfg.head_dim,
                        "seq_len": cfg.seq_len, "top_k": cfg.top_k, "window": cfg.window,
+                       "seq_lens": ("ragged: seeded uniform [L/8, L], mean %.0f" % (sum(lens) / len(lens))
+                                    if args.ragged else "uniform L"),
                        "kv_layout": (f"paged: {args.paged}-token HND pages, random placement"
                                      if args.paged else "dense [B][Hkv][L][D]"),
                        "parallelism": f"kv-head shard x{world}" if shards == world else

@@ -246,6 +246,42 @@ ASP_API asp_status asyncspade_sparse_decode_paged(const asp_decode_params *p, co
                                           float *out, void *workspace, size_t workspace_bytes,
                                           asp_stream stream);
 
+/* ------------------------------------------------------------------------
+ * Quest-style page-bound selector -- the in-framework COMPARATOR of SURVEY
+ * §8(f) NEXT-4: the paper's baseline (Quest, page size 16; P:78, P:356,
+ * P:461-465) selects whole pages by an upper bound of the attention logit,
+ * with the CURRENT query (so on the critical path).  SPEC's
+ * page_level_select is the definition:
+ *   tokens of row (b, h) are cut into consecutive pages of page_size (the
+ *   last one may be short); per page and dimension the key max / min over
+ *   its tokens are kept; the page bound is
+ *     U = max_g sum_d max(q[b,hG+g,d] * maxK_d, q[b,hG+g,d] * minK_d)
+ *   (ASP_AGG_SUM: sum_g); the top_k / page_size pages with the largest U
+ *   are taken (ties to the lower page) and sel_idx[b,h,:] lists all their
+ *   tokens in ascending order, -1 for positions past seq_lens[b] and for
+ *   missing pages (fewer pages than top_k / page_size: ASP_FLAG_SHORT_ROW).
+ * p         as asyncspade_score_select (dense strided K; top_k must be a
+ *           multiple of page_size, else ASP_ERR_SHAPE).  1 <= page_size <= 128.
+ * meta      device, >= asyncspade_quest_meta_bytes(p, page_size) bytes,
+ *           16-B aligned: the page extremes, written by summarize (bf16,
+ *           exact) and read by select.  In a serving engine it is
+ *           maintained at KV append time; here it is rebuilt from the cache.
+ * q         device fp32 [batch][n_q_heads][head_dim] (the current query).
+ * sel_idx   device int32 [batch][n_kv_heads][top_k], written.
+ * workspace >= asyncspade_quest_select_workspace(p, page_size), 256-B aligned.
+ * Precision: fp32 FMA of the exact bf16 extremes (the bound is exact to
+ * ~1e-6 relative); deterministic per row.
+ * ---------------------------------------------------------------------- */
+ASP_API size_t asyncspade_quest_meta_bytes(const asp_select_params *p, int32_t page_size);
+ASP_API asp_status asyncspade_quest_summarize(const asp_select_params *p, int32_t page_size,
+                                      const asp_bf16 *k_cache, const int32_t *seq_lens,
+                                      void *meta, asp_stream stream);
+ASP_API size_t asyncspade_quest_select_workspace(const asp_select_params *p, int32_t page_size);
+ASP_API asp_status asyncspade_quest_select(const asp_select_params *p, int32_t page_size,
+                                   const float *q, const void *meta, const int32_t *seq_lens,
+                                   int32_t *sel_idx, void *workspace, size_t workspace_bytes,
+                                   uint32_t *dev_flags, asp_stream stream);
+
 /* Human-readable name of a status code (static storage). */
 ASP_API const char *asyncspade_status_string(asp_status s);
 /* ASYNCSPADE_ABI_VERSION the library was built with. */

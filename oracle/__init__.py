@@ -61,6 +61,8 @@ def _load():
         lib.asp_oracle_predict.restype = u32
         lib.asp_oracle_score.argtypes = [i32, i32, i32, i32, i32, vp, vp, vp, i32, vp]
         lib.asp_oracle_score.restype = u32
+        lib.asp_oracle_page_bounds.argtypes = [i32, i32, i32, i32, i32, i32, vp, vp, vp, i32, vp]
+        lib.asp_oracle_page_bounds.restype = u32
         lib.asp_oracle_select.argtypes = [i32, i32, vp, vp, i32, vp]
         lib.asp_oracle_select.restype = u32
         lib.asp_oracle_sparse_decode.argtypes = [i32, i32, i32, i32, i32, i32, i32, f64,
@@ -161,6 +163,45 @@ def dense_attention(q: np.ndarray, k_cache: np.ndarray, v_cache: np.ndarray, seq
     _load().asp_oracle_dense_attention(B, Hq, Hkv, D, L, float(sm_scale), _p(sl), _p(qq),
                                        _p(k), _p(v), _p(out))
     return out
+
+
+def page_bounds(q: np.ndarray, k_cache: np.ndarray, seq_lens, page_size: int, agg: int = AGG_MAX):
+    """Quest comparator: per-page upper bounds of q . k (SPEC page_level_select,
+    S:392-400; the paper's Quest baseline P:356).  q fp32 [B, Hq, D]; k_cache
+    bf16 bits [B, Hkv, L, D].  Returns (fp64 [B, Hkv, ceil(L / P)], bits)."""
+    qq = _c(q, np.float32)
+    k = _c(k_cache, np.uint16)
+    B, Hq, D = qq.shape
+    _, Hkv, L, _ = k.shape
+    NP = (L + page_size - 1) // page_size
+    sl = _c(np.broadcast_to(np.asarray(seq_lens), (B,)), np.int32)
+    out = np.empty((B, Hkv, NP), np.float64)
+    cond = _load().asp_oracle_page_bounds(B, Hq, Hkv, D, L, page_size, _p(sl), _p(qq), _p(k),
+                                          agg, _p(out))
+    return out, int(cond)
+
+
+def quest_select(q: np.ndarray, k_cache: np.ndarray, seq_lens, top_k: int, page_size: int,
+                 agg: int = AGG_MAX):
+    """Quest comparator, SPEC page_level_select: the top_k /
+    page_size pages with the largest bound (ties to the lower page, the
+    token selector's rule) and all their tokens, ascending; positions past
+    the row's length and missing pages are -1.  Returns (idx int32
+    [B, Hkv, top_k], page idx, bounds)."""
+    B = q.shape[0]
+    Hkv = k_cache.shape[1]
+    bounds, _ = page_bounds(q, k_cache, seq_lens, page_size, agg)
+    lens = np.broadcast_to(np.asarray(seq_lens), (B,))
+    n_pages = (lens + page_size - 1) // page_size
+    pidx, _ = select(bounds, top_k // page_size, np.repeat(n_pages, Hkv).reshape(B, Hkv))
+    idx = np.full((B, Hkv, top_k), -1, np.int32)
+    for b in range(B):
+        for h in range(Hkv):
+            for e in range(top_k):
+                pg = pidx[b, h, e // page_size]
+                t = pg * page_size + e % page_size if pg >= 0 else -1
+                idx[b, h, e] = t if t < lens[b] else -1
+    return idx, pidx, bounds
 
 
 def step(q_window, q, k_cache, v_cache, seq_lens, top_k, eps=1e-2, flags=0, n_fresh=0,

@@ -272,6 +272,61 @@ uint32_t asp_oracle_score(int32_t B, int32_t Hq, int32_t Hkv, int32_t D, int32_t
 }
 
 /* ------------------------------------------------------------------------
+ * Quest comparator: page upper bounds, SPEC
+ * page_level_select, the paper's Quest baseline at page size 16
+ * (P:356).  Tokens [0, len) of row (b, h) are cut into
+ * consecutive pages of P (the last one may be short); for page j,
+ *   maxK_d = max over its tokens of K[d],  minK_d = min over its tokens,
+ *   U_g = sum_d max(q_gd * maxK_d, q_gd * minK_d),
+ * reduced over the group like the token score (max, or sum with agg = 1).
+ * Output bounds[b][h][j] for j < ceil(len / P), -inf beyond.
+ * ---------------------------------------------------------------------- */
+uint32_t asp_oracle_page_bounds(int32_t B, int32_t Hq, int32_t Hkv, int32_t D, int32_t L_cap,
+                                int32_t P, const int32_t *seq_lens, const float *q,
+                                const uint16_t *k_cache, int32_t agg, double *bounds) {
+    const int G = Hq / Hkv;
+    const int NP = (L_cap + P - 1) / P;
+    uint32_t cond = 0;
+    double *mx = (double *)malloc(sizeof(double) * D), *mn = (double *)malloc(sizeof(double) * D);
+    for (int b = 0; b < B; b++)
+        for (int h = 0; h < Hkv; h++) {
+            double *brow = bounds + ((size_t)b * Hkv + h) * NP;
+            for (int j = 0; j < NP; j++) {
+                const int t0 = j * P;
+                int t1 = t0 + P;
+                if (t1 > seq_lens[b]) t1 = seq_lens[b];
+                if (t0 >= t1) { brow[j] = -INFINITY; continue; }
+                for (int d = 0; d < D; d++) { mx[d] = -INFINITY; mn[d] = INFINITY; }
+                for (int t = t0; t < t1; t++) {
+                    const uint16_t *kr = k_cache + (((size_t)b * Hkv + h) * L_cap + t) * D;
+                    for (int d = 0; d < D; d++) {
+                        const double v = bf16_to_double(kr[d]);
+                        if (v > mx[d]) mx[d] = v;
+                        if (v < mn[d]) mn[d] = v;
+                    }
+                }
+                double best = 0.0;
+                for (int g = 0; g < G; g++) {
+                    const float *qg = q + ((size_t)b * Hq + (size_t)h * G + g) * D;
+                    double u = 0.0;
+                    for (int d = 0; d < D; d++) {
+                        const double a = (double)qg[d] * mx[d], c = (double)qg[d] * mn[d];
+                        u += a > c ? a : c;
+                    }
+                    if (g == 0) best = u;
+                    else if (agg == 1) best += u;
+                    else if (u > best) best = u;
+                }
+                if (!isfinite(best)) cond |= OR_FLAG_NONFINITE;
+                brow[j] = best;
+            }
+        }
+    free(mx);
+    free(mn);
+    return cond;
+}
+
+/* ------------------------------------------------------------------------
  * a3 select: per row, the k tokens with the largest score (P:191, P:267
  * item (2)).  Definition: sort the row by (score descending, index
  * ascending) -- lower index wins ties (reading R9) -- take the first k,

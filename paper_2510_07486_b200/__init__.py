@@ -33,6 +33,8 @@ EXPORTED_SYMBOLS = (
     "asyncspade_predict_query", "asyncspade_score_select_workspace", "asyncspade_score_select",
     "asyncspade_sparse_decode_workspace", "asyncspade_sparse_decode",
     "asyncspade_score_select_paged", "asyncspade_sparse_decode_paged",
+    "asyncspade_quest_meta_bytes", "asyncspade_quest_summarize",
+    "asyncspade_quest_select_workspace", "asyncspade_quest_select",
     "asyncspade_status_string", "asyncspade_abi_version",
 )
 
@@ -108,6 +110,17 @@ def lib() -> ctypes.CDLL:
                                                      ctypes.POINTER(PagedKV), vp, vp, vp, vp, vp,
                                                      vp, vp, vp, sz, vp]
         L.asyncspade_sparse_decode_paged.restype = ctypes.c_int32
+        L.asyncspade_quest_meta_bytes.argtypes = [ctypes.POINTER(SelectParams), ctypes.c_int32]
+        L.asyncspade_quest_meta_bytes.restype = sz
+        L.asyncspade_quest_summarize.argtypes = [ctypes.POINTER(SelectParams), ctypes.c_int32,
+                                                 vp, vp, vp, vp]
+        L.asyncspade_quest_summarize.restype = ctypes.c_int32
+        L.asyncspade_quest_select_workspace.argtypes = [ctypes.POINTER(SelectParams),
+                                                        ctypes.c_int32]
+        L.asyncspade_quest_select_workspace.restype = sz
+        L.asyncspade_quest_select.argtypes = [ctypes.POINTER(SelectParams), ctypes.c_int32, vp, vp,
+                                              vp, vp, vp, sz, vp, vp]
+        L.asyncspade_quest_select.restype = ctypes.c_int32
         L.asyncspade_status_string.argtypes = [ctypes.c_int32]
         L.asyncspade_status_string.restype = ctypes.c_char_p
         L.asyncspade_abi_version.argtypes = []
@@ -327,3 +340,42 @@ def page_pool(cache: torch.Tensor, page_size: int, generator: torch.Generator | 
                                                                                  page_size, D)
     pool[block_table.view(-1).long()] = src
     return pool, block_table
+
+
+# --------------------------------------------------------------------------- Quest comparator
+def quest_summarize(k_cache: torch.Tensor, seq_lens: torch.Tensor, page_size: int, top_k: int,
+                    n_q_heads: int, *, meta: torch.Tensor | None = None,
+                    stream=None) -> torch.Tensor:
+    """Page extremes of a dense K cache -> asyncspade_quest_summarize."""
+    B, Hkv, L, D = k_cache.shape
+    p = SelectParams(B, n_q_heads, Hkv, D, top_k, L, AGG_MAX, *k_cache.stride()[:3])
+    if meta is None:
+        meta = torch.empty(max(int(lib().asyncspade_quest_meta_bytes(ctypes.byref(p), page_size)),
+                               256), dtype=torch.uint8, device=k_cache.device)
+    _check(lib().asyncspade_quest_summarize(ctypes.byref(p), page_size, _ptr(_u16(k_cache)),
+                                            _ptr(seq_lens), _ptr(meta), _stream(stream)),
+           "asyncspade_quest_summarize")
+    return meta
+
+
+def quest_select(q: torch.Tensor, meta: torch.Tensor, k_cache: torch.Tensor,
+                 seq_lens: torch.Tensor, top_k: int, page_size: int, *,
+                 sel_idx: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+                 aggregation: int = AGG_MAX, dev_flags: torch.Tensor | None = None,
+                 stream=None) -> torch.Tensor:
+    """Quest page-bound selection -> asyncspade_quest_select.  q fp32
+    [B, Hq, D]; returns token indices int32 [B, Hkv, top_k] (whole pages)."""
+    B, Hq, D = q.shape
+    _, Hkv, L, _ = k_cache.shape
+    p = SelectParams(B, Hq, Hkv, D, top_k, L, aggregation, *k_cache.stride()[:3])
+    if sel_idx is None:
+        sel_idx = torch.empty(B, Hkv, top_k, dtype=torch.int32, device=q.device)
+    if workspace is None:
+        workspace = _workspace(int(lib().asyncspade_quest_select_workspace(ctypes.byref(p),
+                                                                          page_size)), q.device)
+    ws_bytes = workspace.numel() * workspace.element_size()
+    _check(lib().asyncspade_quest_select(ctypes.byref(p), page_size, _ptr(q), _ptr(meta),
+                                         _ptr(seq_lens), _ptr(sel_idx), _ptr(workspace), ws_bytes,
+                                         _ptr(dev_flags), _stream(stream)),
+           "asyncspade_quest_select")
+    return sel_idx

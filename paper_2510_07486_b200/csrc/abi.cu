@@ -195,6 +195,46 @@ asp_status asyncspade_sparse_decode_paged(const asp_decode_params *p, const asp_
                                        block_table));
 }
 
+size_t asyncspade_quest_meta_bytes(const asp_select_params *p, int32_t page_size) {
+    if (check_select(p) != ASP_OK || page_size < 1 || page_size > 128) return 0;
+    return align256(asp_quest_meta_bytes(*p, page_size));
+}
+
+asp_status asyncspade_quest_summarize(const asp_select_params *p, int32_t page_size,
+                                      const asp_bf16 *k_cache, const int32_t *seq_lens, void *meta,
+                                      asp_stream stream) {
+    asp_status st = check_select(p);
+    if (st != ASP_OK) return st;
+    if (page_size < 1 || page_size > 128) return ASP_ERR_UNSUPPORTED;
+    if (!k_cache || !seq_lens || !meta) return ASP_ERR_INVALID_ARGUMENT;
+    if (!aligned16(k_cache) || !aligned16(meta)) return ASP_ERR_INVALID_ARGUMENT;
+    return from_cuda(asp_launch_quest_summarize(*p, page_size, k_cache, seq_lens, meta,
+                                                (cudaStream_t)stream));
+}
+
+size_t asyncspade_quest_select_workspace(const asp_select_params *p, int32_t page_size) {
+    if (check_select(p) != ASP_OK || page_size < 1 || page_size > 128 || p->top_k % page_size)
+        return 0;
+    return align256(asp_quest_workspace_bytes(*p, page_size));
+}
+
+asp_status asyncspade_quest_select(const asp_select_params *p, int32_t page_size, const float *q,
+                                   const void *meta, const int32_t *seq_lens, int32_t *sel_idx,
+                                   void *workspace, size_t workspace_bytes, uint32_t *dev_flags,
+                                   asp_stream stream) {
+    asp_status st = check_select(p);
+    if (st != ASP_OK) return st;
+    if (page_size < 1 || page_size > 128) return ASP_ERR_UNSUPPORTED;
+    if (p->top_k % page_size) return ASP_ERR_SHAPE;
+    if (!q || !meta || !seq_lens || !sel_idx) return ASP_ERR_INVALID_ARGUMENT;
+    if (!aligned16(q) || !aligned16(meta)) return ASP_ERR_INVALID_ARGUMENT;
+    if (!workspace || workspace_bytes < asyncspade_quest_select_workspace(p, page_size))
+        return ASP_ERR_WORKSPACE;
+    if (reinterpret_cast<uintptr_t>(workspace) & 255u) return ASP_ERR_WORKSPACE;
+    return from_cuda(asp_launch_quest_select(*p, page_size, q, meta, seq_lens, sel_idx, workspace,
+                                             dev_flags, (cudaStream_t)stream));
+}
+
 const char *asyncspade_status_string(asp_status s) {
     switch (s) {
         case ASP_OK: return "ASP_OK";

@@ -109,4 +109,13 @@ cudaError_t asp_launch_decode(const asp_decode_params &p, const asp_bf16 *q,
                               const int32_t *seq_lens, const int32_t *sel_idx, float *out,
                               float *partials, cudaStream_t s,
                               const asp_paged_kv *pk = nullptr, const int32_t *block_table = nullptr);
+// Quest-style page-bound comparator (quest.cu)
+size_t asp_quest_meta_bytes(const asp_select_params &p, int page_size);
+size_t asp_quest_workspace_bytes(const asp_select_params &p, int page_size);
+cudaError_t asp_launch_quest_summarize(const asp_select_params &p, int page_size,
+                                       const asp_bf16 *k_cache, const int32_t *seq_lens,
+                                       void *meta, cudaStream_t s);
+cudaError_t asp_launch_quest_select(const asp_select_params &p, int page_size, const float *q,
+                                    const void *meta, const int32_t *seq_lens, int32_t *sel_idx,
+                                    void *workspace, uint32_t *dev_flags, cudaStream_t s);
 int asp_sm_count();

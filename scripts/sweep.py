@@ -3,6 +3,7 @@
     python scripts/sweep.py long-cot          # [3] batch 8, ctx 4k..512k, per-GPU shard of P = 8
     python scripts/sweep.py high-concurrency  # [4] Qwen3-8B shape, ctx 4k, batch 1..512, a5 overlap
     python scripts/sweep.py layer-packed      # NEXT-2: P_l layers per launch (small shapes)
+    python scripts/sweep.py quest             # NEXT-4: Quest page-bound comparator vs AsyncSpade
 
 One JSON line per point.  Times are CUDA events on the launching stream over
 `--steps` back-to-back steps after `--warmup`, per step in µs.  Core bytes as
@@ -19,6 +20,7 @@ layer parameters) on the main stream:
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import sys
@@ -97,9 +99,63 @@ def point(cfg, args, kv_heads=None, overlap=False):
     return res
 
 
+def quest_point(cfg, args, P=16):
+    step = DecodeStep(cfg, "cuda")
+    step.fill_synthetic()
+    torch.cuda.synchronize()
+    B, Hkv, L, D, k = cfg.batch, cfg.n_kv_heads, cfg.seq_len, cfg.head_dim, cfg.top_k
+    q32 = step.q.float()
+    meta = asp.quest_summarize(step.k_cache, step.seq_lens, P, k, cfg.n_q_heads)
+    ws = torch.empty(max(int(asp.lib().asyncspade_quest_select_workspace(
+        ctypes.byref(asp.SelectParams(B, cfg.n_q_heads, Hkv, D, k, L, 0,
+                                      *step.k_cache.stride()[:3])), P)), 256),
+                     dtype=torch.uint8, device="cuda")
+    idx_q = torch.empty_like(step.sel_idx)
+
+    def quest_step():
+        asp.quest_select(q32, meta, step.k_cache, step.seq_lens, k, P, sel_idx=idx_q,
+                         workspace=ws)
+        asp.sparse_decode(step.q, step.k_cache, step.v_cache, step.seq_lens, idx_q, out=step.out,
+                          workspace=step.ws_dec, params=step.p_dec)
+
+    t_asp = timed(step.run, args.steps, args.warmup)
+    t_quest = timed(quest_step, args.steps, args.warmup)
+    t_qsel = timed(lambda: asp.quest_select(q32, meta, step.k_cache, step.seq_lens, k, P,
+                                            sel_idx=idx_q, workspace=ws), args.steps, args.warmup)
+    t_sum = timed(lambda: asp.quest_summarize(step.k_cache, step.seq_lens, P, k, cfg.n_q_heads,
+                                              meta=meta), 3, 1)
+    # selection quality: overlap with the exact token top-k of the current query
+    step.run()
+    exact = asp.score_select(q32, step.k_cache, step.seq_lens, k)
+    quest_step()
+    torch.cuda.synchronize()
+
+    def overlap(a):
+        n = 0
+        ea, eb = a.view(-1, k).cpu(), exact.view(-1, k).cpu()
+        for r in range(ea.shape[0]):
+            n += len(set(ea[r].tolist()) & set(eb[r].tolist()))
+        return n / (ea.shape[0] * k)
+
+    meta_bytes = B * Hkv * ((L + P - 1) // P) * 2 * D * 2
+    kv_sel = 2 * B * Hkv * k * D * 2
+    res = {"workload": cfg.name, "page_size": P, "asyncspade_step_us": t_asp,
+           "quest_step_us": t_quest, "quest_select_us": t_qsel, "quest_summarize_us": t_sum,
+           "quest_bytes_per_step": meta_bytes + kv_sel,
+           "asyncspade_bytes_per_step": cfg.core_bytes(),
+           "quest_select_tb_per_s": meta_bytes / (t_qsel * 1e-6) / 1e12,
+           "overlap_with_exact_topk": {"asyncspade_predicted_query": overlap(step.sel_idx),
+                                       "quest_current_query": overlap(idx_q)},
+           "note": "Quest runs on the critical path (current query); AsyncSpade's selection "
+                   "can run a step ahead (a5); synthetic N(0,1) keys, AR(1) queries"}
+    del step
+    torch.cuda.empty_cache()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("sweep", choices=["long-cot", "high-concurrency", "layer-packed"])
+    ap.add_argument("sweep", choices=["long-cot", "high-concurrency", "layer-packed", "quest"])
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--out", default=None)
@@ -110,6 +166,15 @@ def main():
         for e in range(12, 20):                                # 4k .. 512k
             cfg = configs.long_cot(1 << e)
             lines.append(point(cfg, args, kv_heads=(0, 1)))     # per-GPU shard at P = 8
+            print(json.dumps(lines[-1]), flush=True)
+    elif args.sweep == "quest":
+        # NEXT-4 comparator: Quest selects
+        # pages of 16 by an upper bound with the CURRENT query (critical path);
+        # AsyncSpade selects tokens with the predicted query.  Step times and the
+        # overlap ratio (Eq. 1) of each selection with the exact
+        # token top-k of the current query.
+        for cfg in (configs.QWEN3_8B, configs.QWEN3_32B):
+            lines.append(quest_point(cfg, args))
             print(json.dumps(lines[-1]), flush=True)
     elif args.sweep == "layer-packed":
         # NEXT-2: per-layer step time when P_l layers share one

@@ -519,3 +519,35 @@ def test_paged_matches_dense_bit_for_bit(G, D, P):
     o_or = oracle.sparse_decode(from_dev_bf16(q[b:b + 1]), K[b:b + 1], V[b:b + 1],
                                 idx_p[b:b + 1].cpu().numpy(), [lens[b]], n_fresh=1)
     assert rel_inf_err(out_p[b:b + 1].cpu().numpy(), o_or) <= ATTN_RTOL
+
+
+# ----------------------------------------------------------------------------- Quest comparator
+@pytest.mark.parametrize("G,D,agg", [(8, 128, asp.AGG_MAX), (1, 64, asp.AGG_MAX), (4, 128, asp.AGG_SUM)])
+def test_quest_select_parity(G, D, agg):
+    """GPU Quest page-bound selection vs the oracle (SPEC page_level_select):
+    page sets equal outside the 1e-5 band of the k/P-th bound, every selected
+    page expanded to its tokens (ascending, -1 past the length)."""
+    B, Hkv, L, P, k = 3, 2, 1000, 16, 128
+    seed = synth.base_seed(0) + 313 + G
+    K = synth.kv_cache(seed, synth.STREAM_K, B, Hkv, L, D)
+    Kd = to_dev_bf16(K)
+    lens = [1000, 517, 40]
+    sl = torch.tensor(lens, dtype=torch.int32, device=DEV)
+    q = (np.random.default_rng(seed).standard_normal((B, Hkv * G, D))).astype(np.float32)
+    meta = asp.quest_summarize(Kd, sl, P, k, Hkv * G)
+    flags = torch.zeros(1, dtype=torch.int32, device=DEV)
+    idx = asp.quest_select(torch.from_numpy(q).to(DEV), meta, Kd, sl, k, P, aggregation=agg,
+                           dev_flags=flags).cpu().numpy()
+    _, pidx_or, bounds = oracle.quest_select(q, K, lens, k, P, agg)
+    for b in range(B):
+        npg = (lens[b] + P - 1) // P
+        for h in range(Hkv):
+            row = idx[b, h]
+            pages = row[::P]
+            pages = np.where(pages >= 0, pages // P, -1)
+            check_selection(pages, bounds[b, h], npg, k // P)
+            # expansion: whole pages, ascending, -1 past the length
+            exp = np.array([pg * P + e % P if pg >= 0 and pg * P + e % P < lens[b] else -1
+                            for e, pg in enumerate(np.repeat(pages, P))])
+            np.testing.assert_array_equal(row, exp)
+    assert flags.item() & asp.FLAG_SHORT_ROW              # row b = 2 has 3 pages < 8

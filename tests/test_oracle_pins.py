@@ -404,3 +404,73 @@ def test_generator_determinism_and_sharding():
     np.testing.assert_array_equal(q1[:, 4:], q2)
     x = synth.bf16_bits_to_f32(synth.kv_cache(s, synth.STREAM_V, 4, 8, 512, 128))
     assert abs(float(x.mean())) < 0.01 and abs(float(x.std()) - 1.0) < 0.01
+
+
+# ----------------------------------------------------------------------------- Quest comparator
+def _quest_case(seed, B=2, Hq=4, Hkv=2, D=16, L=64):
+    rng = np.random.default_rng(seed)
+    q = rng.standard_normal((B, Hq, D)).astype(np.float32)
+    K = synth.kv_cache(seed, synth.STREAM_K, B, Hkv, L, D)
+    return q, K
+
+
+def test_quest_page_size_one_is_token_topk():
+    """SPEC S:395 example 1: P = 1 -> the page bound is the exact dot product
+    and the selection equals token-level top-k."""
+    q, K = _quest_case(3)
+    lens = [64, 37]
+    idx, _, bounds = oracle.quest_select(q, K, lens, 8, 1)
+    s, _ = oracle.score(q, K, lens)
+    np.testing.assert_array_equal(bounds[:, :, :37], s[:, :, :37])
+    ref, _ = oracle.select(s, 8, np.repeat(lens, 2).reshape(2, 2))
+    np.testing.assert_array_equal(idx, ref)
+
+
+def test_quest_bound_brute_force_and_upper_bound_property():
+    """every token's true score is <= its page's bound
+    (checked exhaustively over every token of every page), and the C bound
+    matches an independent numpy min / max reduction of the decoded keys."""
+    q, K = _quest_case(5, L=80)
+    P = 16
+    lens = [80, 70]
+    bounds, _ = oracle.page_bounds(q, K, lens, P)
+    s, _ = oracle.score(q, K, lens)
+    kv = K.astype(np.uint32) << 16
+    kf = kv.view(np.float32).astype(np.float64)
+    for b in range(2):
+        for h in range(2):
+            for j in range((lens[b] + P - 1) // P):
+                t0, t1 = j * P, min(lens[b], (j + 1) * P)
+                assert np.all(s[b, h, t0:t1] <= bounds[b, h, j] + 1e-12)
+                mx, mn = kf[b, h, t0:t1].max(0), kf[b, h, t0:t1].min(0)
+                qg = q[b, 2 * h:2 * h + 2].astype(np.float64)
+                u = np.maximum(qg * mx, qg * mn).sum(1).max()
+                assert abs(u - bounds[b, h, j]) <= 1e-12 * max(1.0, abs(u))
+            assert np.all(np.isneginf(bounds[b, h, (lens[b] + P - 1) // P:]))
+
+
+def test_quest_constant_pages_select_whole_token_pages():
+    """SPEC S:396 example 2: keys identical within every page -> the bound is
+    the exact token score, and the selected pages are the pages of the
+    token-level selection (page-aligned budget)."""
+    rng = np.random.default_rng(11)
+    B, Hq, Hkv, D, L, P = 1, 2, 1, 8, 64, 8
+    per_page = rng.standard_normal((B, Hkv, L // P, D)).astype(np.float32)
+    Kf = np.repeat(per_page, P, axis=2)
+    K = (Kf.view(np.uint32) >> 16).astype(np.uint16)            # exact bf16 truncation
+    q = rng.standard_normal((B, Hq, D)).astype(np.float32)
+    idx, pidx, bounds = oracle.quest_select(q, K, [L], 16, P)
+    s, _ = oracle.score(q, K, [L])
+    np.testing.assert_allclose(bounds[0, 0], s[0, 0, ::P], rtol=0, atol=0)
+    tok, _ = oracle.select(s, 16)
+    assert set(tok[0, 0] // P) == set(pidx[0, 0])
+    np.testing.assert_array_equal(np.sort(idx[0, 0]), np.sort(
+        np.concatenate([np.arange(pg * P, pg * P + P) for pg in sorted(pidx[0, 0])])))
+
+
+def test_quest_short_rows_and_partial_last_page():
+    """Tokens past the length are -1; fewer pages than the budget pad -1."""
+    q, K = _quest_case(9, B=1, Hkv=1, Hq=1, L=64)
+    idx, pidx, _ = oracle.quest_select(q, K, [20], 48, 16)     # 2 pages exist, 3 wanted
+    assert list(pidx[0, 0]) == [0, 1, -1]
+    np.testing.assert_array_equal(idx[0, 0], np.r_[np.arange(20), -np.ones(28, int)])

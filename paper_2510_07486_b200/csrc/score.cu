@@ -247,8 +247,55 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long total = (long)p.batch * p.n_kv_heads * tiles_per_row;
     TileIter it;
-    it.start = total * blockIdx.x / gridDim.x;
-    it.end = total * (blockIdx.x + 1) / gridDim.x;
+    // Balance the VALID tiles (token base < row length), not the capacity: CTA
+    // i takes valid tiles [i T / grid, (i+1) T / grid), mapped back to the
+    // flattened (row, tile) capacity index the iterator walks (it skips the
+    // invalid tiles in between).  Ragged batches would otherwise leave the
+    // CTAs over short rows idle.  (seq_lens is caller-written: no PDL wait.)
+    __shared__ long long s_rng[2];
+    if (warp == 3) {
+        const int tpr = tiles_per_row, Hkv = p.n_kv_heads;
+        auto vt = [&](int b) {                        // valid tiles of each row of batch b
+            const int len = min(max(seq_lens[b], 0), p.max_seq_len);
+            return (len + kTileM - 1) / kTileM;
+        };
+        long long T = 0;                              // all valid tiles
+        for (int b0 = 0; b0 < p.batch; b0 += 32) {
+            long long v = b0 + lane < p.batch ? (long long)vt(b0 + lane) * Hkv : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            T += v;
+        }
+        // capacity index of valid tile number v (v == T -> total)
+        auto locate = [&](long long v) -> long long {
+            if (v >= T) return total;
+            long long before = 0;
+            for (int b0 = 0; b0 < p.batch; b0 += 32) {
+                const int b = b0 + lane;
+                const int n = b < p.batch ? vt(b) : 0;
+                long long inc = (long long)n * Hkv;   // inclusive scan over the chunk
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const long long t = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += t;
+                }
+                const unsigned hit = __ballot_sync(0xffffffffu, b < p.batch && before + inc > v);
+                if (hit) {
+                    const int l = __ffs(hit) - 1;
+                    const long long excl = __shfl_sync(0xffffffffu, inc, l) - (long long)__shfl_sync(0xffffffffu, n, l) * Hkv;
+                    const int nb = __shfl_sync(0xffffffffu, n, l);
+                    const long long off = v - before - excl;
+                    const long long h = off / nb, j = off % nb;
+                    return ((long long)(b0 + l) * Hkv + h) * tpr + j;
+                }
+                before += __shfl_sync(0xffffffffu, inc, 31);
+            }
+            return total;
+        };
+        const long long a = locate(T * blockIdx.x / gridDim.x);
+        const long long e = locate(T * (blockIdx.x + 1) / gridDim.x);
+        if (lane == 0) { s_rng[0] = a; s_rng[1] = e; }
+    }
     it.tpr = tiles_per_row;
     it.n_kv = p.n_kv_heads;
     it.seq_lens = seq_lens;
@@ -266,7 +313,12 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder_g;
-    asp::pdl_wait();                        // q_hat, seq_lens and the score buffer are ours now
+    it.start = s_rng[0];
+    it.end = s_rng[1];
+    // PDL: of this kernel's inputs only q_hat comes from the preceding kernel
+    // (predict), so the K stream starts at once; the B builder waits before it
+    // reads q_hat and the epilogue before its first store (an earlier reader of
+    // the score buffer -- the previous select -- has then completed too).
     asp::pdl_trigger();
 #ifdef ASP_PROFILE_SCORE
     const long long t_kernel0 = clock64();
@@ -426,6 +478,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
         __syncwarp();
     } else if (warp == 2) {
         // ------------------------------------------------ B-operand builder
+        asp::pdl_wait();
         int bs = -1;
         uint32_t bph = 0;
         int cur_row = -1;
@@ -475,6 +528,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
         }
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue: TMEM -> scores
+        asp::pdl_wait();
         // two warpgroups alternate tiles (each warp drains its 32-lane quadrant)
         const int quad = warp & 3;                  // TMEM lanes 32*quad .. +31
         const int group = (warp - 4) >> 2;

@@ -254,8 +254,9 @@ def test_decode_edge_cases():
 
 
 # ----------------------------------------------------------------------------- composed step
-def _oracle_row_checks(step: DecodeStep, rows, n_fresh=0):
-    """For sampled (b, h): predict / select (band) / decode parity, chained."""
+def _oracle_row_checks(step: DecodeStep, rows, n_fresh=0, lens=None):
+    """For sampled (b, h): predict / select (band) / decode parity, chained
+    (lens: per-batch sequence lengths of a ragged step; default uniform L)."""
     cfg = step.cfg
     G, D, L, k, W = cfg.group, cfg.head_dim, cfg.seq_len, cfg.top_k, cfg.window
     seed = synth.base_seed(cfg.index)
@@ -272,9 +273,10 @@ def _oracle_row_checks(step: DecodeStep, rows, n_fresh=0):
         assert rel_inf_err(qh_g[b, hl * G:(hl + 1) * G], qh_or[0]) <= Q_HAT_RTOL
         K = synth.kv_rows(seed, synth.STREAM_K, b, hg, 0, L, cfg.n_kv_heads, L, D)[None, None]
         V = synth.kv_rows(seed, synth.STREAM_V, b, hg, 0, L, cfg.n_kv_heads, L, D)[None, None]
-        s_or, _ = oracle.score(qh_g[b:b + 1, hl * G:(hl + 1) * G], K, [L])   # chained
-        bands += check_selection(idx_g[b, hl], s_or[0, 0], L - n_fresh, k)["band"]
-        o_or = oracle.sparse_decode(q, K, V, idx_g[b:b + 1, hl:hl + 1], [L], n_fresh)
+        n = L if lens is None else int(lens[b])
+        s_or, _ = oracle.score(qh_g[b:b + 1, hl * G:(hl + 1) * G], K, [n])   # chained
+        bands += check_selection(idx_g[b, hl], s_or[0, 0], n - n_fresh, k)["band"]
+        o_or = oracle.sparse_decode(q, K, V, idx_g[b:b + 1, hl:hl + 1], [n], n_fresh)
         assert rel_inf_err(out_g[b, hl * G:(hl + 1) * G], o_or[0]) <= ATTN_RTOL
     return bands
 
@@ -311,6 +313,27 @@ def test_step_qwen3_32b_graph_sampled_rows_and_determinism():
     torch.cuda.synchronize()
     assert torch.equal(idx1, step.sel_idx) and torch.equal(out1, step.out)
     _oracle_row_checks(step, rows_sample(step.cfg.batch * step.n_kv, 8, seed=2))
+    del step
+    torch.cuda.empty_cache()
+
+
+def test_step_qwen3_32b_ragged_sampled_rows():
+    """Config [2] at full size with bench.py --ragged's length mix (seeded
+    uniform in [L/8, L]; the score kernel balances its VALID tiles over the
+    SMs): sampled rows -- the shortest and the longest among them -- vs the
+    oracle."""
+    cfg = configs.QWEN3_32B
+    step = DecodeStep(cfg, DEV)
+    step.fill_synthetic()
+    rng = np.random.default_rng(synth.base_seed(cfg.index) + 99)
+    lens = rng.integers(cfg.seq_len // 8, cfg.seq_len + 1, cfg.batch)
+    step.seq_lens.copy_(torch.from_numpy(lens.astype(np.int32)))
+    step.run()
+    torch.cuda.synchronize()
+    assert int(step.dev_flags.item()) == 0
+    bmin, bmax = int(np.argmin(lens)), int(np.argmax(lens))
+    rows = sorted({bmin * step.n_kv, bmax * step.n_kv + 7, *rows_sample(step.cfg.batch * step.n_kv, 4, seed=5)})
+    _oracle_row_checks(step, rows, lens=lens)
     del step
     torch.cuda.empty_cache()
 

@@ -269,7 +269,7 @@ def main():
         if evs is not None:
             evs[3].record(stream)
 
-    def one_step(evs=None):
+    def one_step(evs=None, out=None):
         if pool is not None:
             return one_step_paged(evs)
         if evs is not None:
@@ -282,7 +282,8 @@ def main():
         if evs is not None:
             evs[2].record(stream)
         asp.sparse_decode(step.q, step.k_cache, step.v_cache, step.seq_lens, step.sel_idx,
-                          out=step.out, workspace=step.ws_dec, params=step.p_dec)
+                          out=step.out if out is None else out, workspace=step.ws_dec,
+                          params=step.p_dec)
         if evs is not None:
             evs[3].record(stream)
 
@@ -337,23 +338,24 @@ def main():
         gather_ms = e0.elapsed_time(e1) / 10
 
     # e2e through the public API with host buffers (pinned): per step H2D of
-    # the new query state q_t (window push, fp32), the current query q (bf16)
-    # and the new token's k/v rows; D2H of the attention output.  The copies
-    # run on a copy stream, double-buffered, overlapped with the previous
-    # step's compute (as a serving loop would); every byte of every step still
-    # crosses PCIe inside the timed region.
+    # the new query state q_t (fp32) and the new token's k/v rows; one a0
+    # kernel (asyncspade_append) puts q_t into the window ring, bf16(q_t) into
+    # the current query and the k/v rows into the caches; the step's decode
+    # writes a double-buffered output that goes D2H.  The copies run on a
+    # copy stream, overlapped with the previous step's compute (as a serving
+    # loop would); every byte of every step still crosses PCIe inside the
+    # timed region.
     e2e = None
     if not (args.no_e2e or args.profile):
         B, nq, D = cfg.batch, step.n_q, cfg.head_dim
         L = cfg.seq_len
         h_qt = [torch.randn(B, nq, D, dtype=torch.float32).pin_memory() for _ in range(2)]
-        h_q = [torch.randn(B, nq, D).to(torch.bfloat16).pin_memory() for _ in range(2)]
         h_kv = [torch.randn(2, B, step.n_kv, D).to(torch.bfloat16).pin_memory() for _ in range(2)]
         h_out = [torch.empty(B, nq, D, dtype=torch.float32).pin_memory() for _ in range(2)]
         d_qt = [torch.empty(B, nq, D, dtype=torch.float32, device="cuda") for _ in range(2)]
-        d_q = [torch.empty(B, nq, D, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
         d_kv = [torch.empty(2, B, step.n_kv, D, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
         d_out = [torch.empty(B, nq, D, dtype=torch.float32, device="cuda") for _ in range(2)]
+        pos = torch.full((B,), L - 1, dtype=torch.int32, device="cuda")
         copy = torch.cuda.Stream()
         h2d_done = [torch.cuda.Event() for _ in range(2)]
         used = [torch.cuda.Event() for _ in range(2)]
@@ -365,21 +367,16 @@ def main():
             with torch.cuda.stream(copy):
                 copy.wait_event(used[b])                   # step i-2 consumed this buffer
                 d_qt[b].copy_(h_qt[b], non_blocking=True)
-                d_q[b].copy_(h_q[b], non_blocking=True)
                 d_kv[b].copy_(h_kv[b], non_blocking=True)
                 h2d_done[b].record(copy)
 
         def e2e_step(i):
             b = i % 2
             stream.wait_event(h2d_done[b])
-            step.push_query(d_qt[b])
-            step.q.copy_(d_q[b])
-            step.k_cache[:, :, L - 1].copy_(d_kv[b][0])
-            step.v_cache[:, :, L - 1].copy_(d_kv[b][1])
-            used[b].record(stream)
-            one_step()
             stream.wait_event(d2h_done[b])                   # step i-2's output left d_out[b]
-            d_out[b].copy_(step.out)
+            step.append(d_qt[b], d_kv[b][0], d_kv[b][1], pos)  # a0: one kernel
+            used[b].record(stream)
+            one_step(out=d_out[b])
             out_ready[b].record(stream)
             with torch.cuda.stream(copy):
                 copy.wait_event(out_ready[b])
@@ -408,11 +405,12 @@ def main():
         tt = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        bi = h_qt[0].numel() * 4 + h_q[0].numel() * 2 + h_kv[0].numel() * 2
+        bi = h_qt[0].numel() * 4 + h_kv[0].numel() * 2
         bo = h_out[0].numel() * 4
         e2e = {"value": float(tt[0]) * 1e3, "unit": UNIT, "h2d_bytes_per_step": bi * world,
                "d2h_bytes_per_step": bo * world,
-               "copies": "pinned host, copy stream, double-buffered, overlapped with compute"}
+               "copies": "pinned host, copy stream, double-buffered, overlapped with compute; "
+                         "a0 (asyncspade_append) puts q_t / k / v into the state in one kernel"}
 
     # a5: the paper's steady state -- selection
     # for step t+1 (predict, score, top-k) on a side stream, overlapped with
@@ -482,6 +480,7 @@ def main():
                          "frac": achieved / peak, "traffic": _traffic(),
                          "algorithmic_bytes_per_launch": k_bytes, "peak_source": peak_src},
             "gpu_launches": 5 * args.steps,
+            "gpu_launches_e2e_per_step": 6,
             "timing": "headline: events around K back-to-back steps; per_call_ms / roofline: a "
                       "second K-step pass with events between the calls",
             "dev_flags": flags,

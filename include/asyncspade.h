@@ -7,6 +7,7 @@
  * path of one attention layer's decode step is four kernels, exposed as
  * three entry points:
  *
+ *   asyncspade_append          a0  new query / K / V into the state
  *   asyncspade_predict_query   a1  q_hat from the query window     (Alg.1 Steps 1-6)
  *   asyncspade_score_select    a2  q_hat . K scores per KV head    (Alg.1 Step 7)
  *                              a3  per-row top-k token selection  (P:191, P:267 item (2))
@@ -95,6 +96,38 @@ enum { ASP_AGG_MAX = 0, ASP_AGG_SUM = 1 };
 
 typedef uint16_t asp_bf16; /* raw bf16 bit pattern */
 typedef void *asp_stream;  /* cudaStream_t */
+
+/* ------------------------------------------------------------------------
+ * a0  asyncspade_append
+ *
+ * The new token of every sequence enters the state the path reads (P:191:
+ * the inference side "enqueues the query state to the sliding window"; the
+ * new key / value join the cache):
+ *   q_window[b][hq][ring_slot][:] = q_t[b][hq][:]             (fp32)
+ *   q_cur[b][hq][:]               = bf16_rn(q_t[b][hq][:])    (nullable)
+ *   K[b][h][pos[b]][:] = k_new[b][h][:], V[b][h][pos[b]][:] = v_new[b][h][:]
+ * One launch (programmatic-dependent after the previous step's kernels)
+ * instead of four strided copies.  The caller then predicts with
+ * ring_start = (ring_slot + 1) % window (the slot written is the newest).
+ *
+ * q_t       device fp32 [batch][n_q_heads][head_dim].
+ * q_window  device fp32 [batch][n_q_heads][window][head_dim] (ring).
+ * q_cur     nullable device bf16 [batch][n_q_heads][head_dim].
+ * k_new, v_new  nullable device bf16 [batch][n_kv_heads][head_dim].
+ * k_cache, v_cache  strided as asp_decode_params' caches (nullable iff the
+ *           matching *_new is).  pos nullable device int32 [batch]: the
+ *           cache position written; rows with pos outside [0, max_seq_len)
+ *           are skipped.  Pure data movement: bit-exact.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    int32_t batch, n_q_heads, n_kv_heads, head_dim, window, ring_slot, max_seq_len;
+    int64_t k_stride_b, k_stride_h, k_stride_t, v_stride_b, v_stride_h, v_stride_t; /* elements */
+} asp_append_params;
+
+ASP_API asp_status asyncspade_append(const asp_append_params *p, const float *q_t, float *q_window,
+                             asp_bf16 *q_cur, const asp_bf16 *k_new, const asp_bf16 *v_new,
+                             asp_bf16 *k_cache, asp_bf16 *v_cache, const int32_t *pos,
+                             asp_stream stream);
 
 /* ------------------------------------------------------------------------
  * a1  asyncspade_predict_query

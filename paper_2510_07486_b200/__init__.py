@@ -30,7 +30,7 @@ SIGN_NEGATED, EPS_ABSOLUTE, NORM_NONE, DOUBLE_SOFTMAX = 1 << 4, 1 << 5, 1 << 6, 
 AGG_MAX, AGG_SUM = 0, 1
 
 EXPORTED_SYMBOLS = (
-    "asyncspade_predict_query", "asyncspade_score_select_workspace", "asyncspade_score_select",
+    "asyncspade_append", "asyncspade_predict_query", "asyncspade_score_select_workspace", "asyncspade_score_select",
     "asyncspade_sparse_decode_workspace", "asyncspade_sparse_decode",
     "asyncspade_score_select_paged", "asyncspade_sparse_decode_paged",
     "asyncspade_quest_meta_bytes", "asyncspade_quest_summarize",
@@ -65,6 +65,16 @@ class DecodeParams(ctypes.Structure):
                 ("v_stride_h", ctypes.c_int64), ("v_stride_t", ctypes.c_int64)]
 
 
+class AppendParams(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("n_q_heads", ctypes.c_int32),
+                ("n_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("window", ctypes.c_int32), ("ring_slot", ctypes.c_int32),
+                ("max_seq_len", ctypes.c_int32),
+                ("k_stride_b", ctypes.c_int64), ("k_stride_h", ctypes.c_int64),
+                ("k_stride_t", ctypes.c_int64), ("v_stride_b", ctypes.c_int64),
+                ("v_stride_h", ctypes.c_int64), ("v_stride_t", ctypes.c_int64)]
+
+
 class PagedKV(ctypes.Structure):
     _fields_ = [("page_size", ctypes.c_int32), ("max_pages_per_seq", ctypes.c_int32),
                 ("num_pages", ctypes.c_int32)]
@@ -90,6 +100,9 @@ def lib() -> ctypes.CDLL:
                 "(there is no CPU fallback)")
         L = ctypes.CDLL(path)
         vp, sz = ctypes.c_void_p, ctypes.c_size_t
+        L.asyncspade_append.argtypes = [ctypes.POINTER(AppendParams), vp, vp, vp, vp, vp, vp, vp,
+                                        vp, vp]
+        L.asyncspade_append.restype = ctypes.c_int32
         L.asyncspade_predict_query.argtypes = [ctypes.POINTER(PredictParams), vp, vp, vp, vp]
         L.asyncspade_predict_query.restype = ctypes.c_int32
         L.asyncspade_score_select_workspace.argtypes = [ctypes.POINTER(SelectParams)]
@@ -196,6 +209,30 @@ def _workspace(nbytes: int, device) -> torch.Tensor:
 
 
 # --------------------------------------------------------------------------- entry points
+def append(q_t: torch.Tensor, q_window: torch.Tensor, ring_slot: int, *,
+           q_cur: torch.Tensor | None = None, k_new: torch.Tensor | None = None,
+           v_new: torch.Tensor | None = None, k_cache: torch.Tensor | None = None,
+           v_cache: torch.Tensor | None = None, pos: torch.Tensor | None = None,
+           stream=None) -> None:
+    """a0 -> asyncspade_append: q_t fp32 [B, Hq, D] into window slot
+    `ring_slot`, bf16(q_t) into q_cur, k_new / v_new [B, Hkv, D] into the
+    caches at pos[b]."""
+    B, Hq, W, D = q_window.shape
+    kc = k_cache if k_cache is not None else v_cache
+    Hkv = kc.shape[1] if kc is not None else 1
+    L = kc.shape[2] if kc is not None else 1
+    ks = k_cache.stride()[:3] if k_cache is not None else (0, 0, 0)
+    vs = v_cache.stride()[:3] if v_cache is not None else (0, 0, 0)
+    p = AppendParams(B, Hq, Hkv, D, W, ring_slot, L, *ks, *vs)
+    _check(lib().asyncspade_append(ctypes.byref(p), _ptr(q_t), _ptr(q_window), _ptr(_u16(q_cur) if q_cur is not None else None),
+                                   _ptr(_u16(k_new) if k_new is not None else None),
+                                   _ptr(_u16(v_new) if v_new is not None else None),
+                                   _ptr(_u16(k_cache) if k_cache is not None else None),
+                                   _ptr(_u16(v_cache) if v_cache is not None else None),
+                                   _ptr(pos), _stream(stream)),
+           "asyncspade_append")
+
+
 def predict_query(q_window: torch.Tensor, q_hat: torch.Tensor | None = None, *, eps: float = 1e-2,
                   flags: int = 0, ring_start: int = 0, dev_flags: torch.Tensor | None = None,
                   stream=None, params: PredictParams | None = None) -> torch.Tensor:

@@ -77,6 +77,28 @@ int asp_sm_count() {
 
 extern "C" {
 
+asp_status asyncspade_append(const asp_append_params *p, const float *q_t, float *q_window,
+                             asp_bf16 *q_cur, const asp_bf16 *k_new, const asp_bf16 *v_new,
+                             asp_bf16 *k_cache, asp_bf16 *v_cache, const int32_t *pos,
+                             asp_stream stream) {
+    if (!p || !q_t || !q_window) return ASP_ERR_INVALID_ARGUMENT;
+    if (p->batch <= 0 || p->n_q_heads <= 0 || p->n_kv_heads <= 0 || p->head_dim <= 0 ||
+        p->window <= 0 || p->max_seq_len <= 0)
+        return ASP_ERR_SHAPE;
+    if (p->ring_slot < 0 || p->ring_slot >= p->window) return ASP_ERR_SHAPE;
+    if (p->head_dim % 8) return ASP_ERR_UNSUPPORTED;
+    if ((k_new && !k_cache) || (v_new && !v_cache) || ((k_new || v_new) && !pos))
+        return ASP_ERR_INVALID_ARGUMENT;
+    if ((p->k_stride_b | p->k_stride_h | p->k_stride_t | p->v_stride_b | p->v_stride_h |
+         p->v_stride_t) & 7)
+        return ASP_ERR_INVALID_ARGUMENT;
+    const void *ptrs[] = {q_t, q_window, q_cur, k_new, v_new, k_cache, v_cache};
+    for (const void *ptr : ptrs)
+        if (ptr && !aligned16(ptr)) return ASP_ERR_INVALID_ARGUMENT;
+    return from_cuda(asp_launch_append(*p, q_t, q_window, q_cur, k_new, v_new, k_cache, v_cache,
+                                       pos, (cudaStream_t)stream));
+}
+
 asp_status asyncspade_predict_query(const asp_predict_params *p, const float *q_window,
                                     float *q_hat, uint32_t *dev_flags, asp_stream stream) {
     if (!p || !q_window || !q_hat) return ASP_ERR_INVALID_ARGUMENT;

@@ -94,6 +94,10 @@ cudaError_t asp_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 
 // Internal launchers (implemented per kernel file, called by abi.cu after
 // host-side validation).  They return cudaGetLastError() of the launch.
+cudaError_t asp_launch_append(const asp_append_params &p, const float *q_t, float *q_window,
+                              asp_bf16 *q_cur, const asp_bf16 *k_new, const asp_bf16 *v_new,
+                              asp_bf16 *k_cache, asp_bf16 *v_cache, const int32_t *pos,
+                              cudaStream_t s);
 cudaError_t asp_launch_predict(const asp_predict_params &p, const float *q_window, float *q_hat,
                                uint32_t *dev_flags, cudaStream_t s);
 // pk / block_table: a paged pool (asyncspade_*_paged), or nullptr (dense cache)

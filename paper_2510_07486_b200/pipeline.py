@@ -46,6 +46,8 @@ class AsyncPipeline:
         self.weights = (torch.zeros(forward_bytes, dtype=torch.uint8, device=dev)
                         if forward_bytes > 0 else None)
         self.sink = torch.zeros(1, dtype=torch.float32, device=dev)
+        self.pos = torch.full((step.cfg.batch * step.layers,), step.cfg.seq_len - 1,
+                              dtype=torch.int32, device=dev)
         self.t = 0
         self.primed = False
 
@@ -67,15 +69,15 @@ class AsyncPipeline:
             synth.synthetic_forward(self.weights, self.sink, stream)
 
     def push(self, q_t=None, kv_t=None) -> None:
-        """a0 on the current stream: q_t into the window ring, the new token's
-        K/V rows into the newest cache slot (len - 1; lengths are held fixed)."""
+        """a0 on the current stream, one kernel (asyncspade_append): q_t into the
+        window ring and (bf16) the current query, the new token's K/V rows into
+        the newest cache slot (len - 1; lengths are held fixed)."""
         s = self.step
         if q_t is not None:
-            s.push_query(q_t)
-        if kv_t is not None:
-            pos = s.cfg.seq_len - 1
-            s.k_cache[:, :, pos].copy_(kv_t[0], non_blocking=True)
-            s.v_cache[:, :, pos].copy_(kv_t[1], non_blocking=True)
+            if kv_t is not None:
+                s.append(q_t, kv_t[0], kv_t[1], self.pos)
+            else:
+                s.append(q_t)
 
     # ------------------------------------------------------------------ pipelined
     def prime(self) -> None:

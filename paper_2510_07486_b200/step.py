@@ -21,7 +21,7 @@ from __future__ import annotations
 
 import torch
 
-from . import (decode_params, predict_params, predict_query, score_select, select_params,
+from . import (append, decode_params, predict_params, predict_query, score_select, select_params,
                sparse_decode, score_select_workspace, sparse_decode_workspace)
 from . import synth
 from .configs import Config
@@ -110,6 +110,19 @@ class DecodeStep:
         self.graph.replay()
 
     # ------------------------------------------------------------------ a0: window push
+    def append(self, q_t: torch.Tensor, k_new: torch.Tensor | None = None,
+               v_new: torch.Tensor | None = None, pos: torch.Tensor | None = None,
+               stream=None) -> None:
+        """a0 in one kernel (asyncspade_append): q_t fp32 [B, n_q, D] becomes the
+        newest window entry and (rounded to bf16) the current query; the new
+        K / V rows [B, n_kv, D] land at pos[b]."""
+        slot = self.ring_start
+        append(q_t, self.window, slot, q_cur=self.q, k_new=k_new, v_new=v_new,
+               k_cache=self.k_cache if k_new is not None else None,
+               v_cache=self.v_cache if v_new is not None else None, pos=pos, stream=stream)
+        self.ring_start = (slot + 1) % self.cfg.window
+        self.p_pred.ring_start = self.ring_start
+
     def push_query(self, q_t: torch.Tensor) -> None:
         """Enqueue q_t (fp32 [B, n_q, D]) as the newest window entry, evicting
         the oldest ("enqueues the query state to the sliding window")."""

@@ -574,3 +574,32 @@ def test_quest_select_parity(G, D, agg):
                             for e, pg in enumerate(np.repeat(pages, P))])
             np.testing.assert_array_equal(row, exp)
     assert flags.item() & asp.FLAG_SHORT_ROW              # row b = 2 has 3 pages < 8
+
+
+# ----------------------------------------------------------------------------- a0 append
+def test_append_is_exact_data_movement():
+    """a0: one kernel writes q_t into the ring slot, bf16(q_t) into
+    the current query and the new K / V rows at pos[b] -- bit for bit what
+    the equivalent torch copies produce; other state untouched; pos < 0
+    skips a row's cache write."""
+    cfg = configs.QWEN3_8B.with_(batch=3, seq_len=512, top_k=64)
+    step = DecodeStep(cfg, DEV)
+    step.fill_synthetic()
+    win0, k0, v0 = step.window.clone(), step.k_cache.clone(), step.v_cache.clone()
+    g = torch.Generator(device="cpu").manual_seed(5)
+    q_t = torch.randn(3, 32, 128, generator=g).to(DEV)
+    k_new = torch.randn(3, 8, 128, generator=g).to(torch.bfloat16).to(DEV)
+    v_new = torch.randn(3, 8, 128, generator=g).to(torch.bfloat16).to(DEV)
+    pos = torch.tensor([511, 7, -1], dtype=torch.int32, device=DEV)
+    slot = step.ring_start
+    step.append(q_t, k_new, v_new, pos)
+    torch.cuda.synchronize()
+    ref_w = win0.clone()
+    ref_w[:, :, slot] = q_t
+    assert torch.equal(step.window, ref_w)
+    assert torch.equal(step.q, q_t.to(torch.bfloat16))
+    ref_k, ref_v = k0.clone(), v0.clone()
+    ref_k[0, :, 511], ref_k[1, :, 7] = k_new[0], k_new[1]
+    ref_v[0, :, 511], ref_v[1, :, 7] = v_new[0], v_new[1]
+    assert torch.equal(step.k_cache, ref_k) and torch.equal(step.v_cache, ref_v)
+    assert step.ring_start == (slot + 1) % cfg.window

@@ -237,6 +237,28 @@ ASP_API asp_status asyncspade_sparse_decode(const asp_decode_params *p, const as
                                     void *workspace, size_t workspace_bytes, asp_stream stream);
 
 /* ------------------------------------------------------------------------
+ * asyncspade_gather_filtered -- the Cache Rank's transfer payload in the
+ * paper's disaggregated design ("the
+ * selected KV entries are then immediately transferred back"; SPEC
+ * gather_filtered): the selected K and V rows packed
+ * contiguously, bit-equal to the cache rows,
+ *     k_out[b][h][j][:] = K[b][h][sel_idx[b][h][j]][:]   (V likewise)
+ * entries that are -1 or >= seq_lens[b] give zero rows, and
+ *     idx_out[b][h][j] = j if 0 <= sel_idx[b][h][j] < seq_lens[b] - n_fresh, else -1
+ * is the selection over the packed rows: the Inference Rank attends with it
+ * over the packed rows plus its own n_fresh newest tokens
+ * (asyncspade_sparse_decode on a [B][Hkv][top_k + n_fresh][D] cache) and
+ * gets exactly the attended set of the single-rank decode.
+ * p         as asyncspade_sparse_decode (sm_scale unused).
+ * k_out, v_out  device bf16 [batch][n_kv_heads][top_k][head_dim], written.
+ * idx_out   nullable device int32 [batch][n_kv_heads][top_k], written.
+ * ---------------------------------------------------------------------- */
+ASP_API asp_status asyncspade_gather_filtered(const asp_decode_params *p, const asp_bf16 *k_cache,
+                                      const asp_bf16 *v_cache, const int32_t *seq_lens,
+                                      const int32_t *sel_idx, asp_bf16 *k_out, asp_bf16 *v_out,
+                                      int32_t *idx_out, asp_stream stream);
+
+/* ------------------------------------------------------------------------
  * Paged KV caches: the block-table layout of paged
  * serving engines, which the paper's baselines run on (P:45, P:78,
  * P:461-465).  The selection itself is unchanged -- token granularity over

@@ -33,6 +33,7 @@ EXPORTED_SYMBOLS = (
     "asyncspade_append", "asyncspade_predict_query", "asyncspade_score_select_workspace", "asyncspade_score_select",
     "asyncspade_sparse_decode_workspace", "asyncspade_sparse_decode",
     "asyncspade_score_select_paged", "asyncspade_sparse_decode_paged",
+    "asyncspade_gather_filtered",
     "asyncspade_quest_meta_bytes", "asyncspade_quest_summarize",
     "asyncspade_quest_select_workspace", "asyncspade_quest_select",
     "asyncspade_status_string", "asyncspade_abi_version",
@@ -103,6 +104,9 @@ def lib() -> ctypes.CDLL:
         L.asyncspade_append.argtypes = [ctypes.POINTER(AppendParams), vp, vp, vp, vp, vp, vp, vp,
                                         vp, vp]
         L.asyncspade_append.restype = ctypes.c_int32
+        L.asyncspade_gather_filtered.argtypes = [ctypes.POINTER(DecodeParams), vp, vp, vp, vp, vp,
+                                                 vp, vp, vp]
+        L.asyncspade_gather_filtered.restype = ctypes.c_int32
         L.asyncspade_predict_query.argtypes = [ctypes.POINTER(PredictParams), vp, vp, vp, vp]
         L.asyncspade_predict_query.restype = ctypes.c_int32
         L.asyncspade_score_select_workspace.argtypes = [ctypes.POINTER(SelectParams)]
@@ -292,6 +296,28 @@ def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
                                           _ptr(out), _ptr(workspace), ws_bytes, _stream(stream)),
            "asyncspade_sparse_decode")
     return out
+
+
+def gather_filtered(k_cache: torch.Tensor, v_cache: torch.Tensor, seq_lens: torch.Tensor,
+                    sel_idx: torch.Tensor, *, n_fresh: int = 0, k_out: torch.Tensor | None = None,
+                    v_out: torch.Tensor | None = None, idx_out: torch.Tensor | None = None,
+                    stream=None, params: DecodeParams | None = None):
+    """The Cache Rank's payload -> asyncspade_gather_filtered: the selected
+    K / V rows packed contiguously [B, Hkv, k, D] (bit-equal) and, if idx_out
+    is given, the selection over the packed rows (j or -1)."""
+    B, Hkv, L, D = k_cache.shape
+    k = sel_idx.shape[-1]
+    p = params or DecodeParams(B, Hkv, Hkv, D, k, n_fresh, L, D ** -0.5, *k_cache.stride()[:3],
+                               *v_cache.stride()[:3])
+    if k_out is None:
+        k_out = torch.empty(B, Hkv, k, D, dtype=k_cache.dtype, device=k_cache.device)
+    if v_out is None:
+        v_out = torch.empty(B, Hkv, k, D, dtype=v_cache.dtype, device=v_cache.device)
+    _check(lib().asyncspade_gather_filtered(ctypes.byref(p), _ptr(_u16(k_cache)), _ptr(_u16(v_cache)),
+                                            _ptr(seq_lens), _ptr(sel_idx), _ptr(_u16(k_out)),
+                                            _ptr(_u16(v_out)), _ptr(idx_out), _stream(stream)),
+           "asyncspade_gather_filtered")
+    return k_out, v_out
 
 
 # --------------------------------------------------------------------------- paged pools

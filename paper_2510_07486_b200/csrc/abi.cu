@@ -257,6 +257,20 @@ asp_status asyncspade_quest_select(const asp_select_params *p, int32_t page_size
                                              dev_flags, (cudaStream_t)stream));
 }
 
+asp_status asyncspade_gather_filtered(const asp_decode_params *p, const asp_bf16 *k_cache,
+                                      const asp_bf16 *v_cache, const int32_t *seq_lens,
+                                      const int32_t *sel_idx, asp_bf16 *k_out, asp_bf16 *v_out,
+                                      int32_t *idx_out, asp_stream stream) {
+    asp_status st = check_decode(p);
+    if (st != ASP_OK) return st;
+    if (!k_cache || !v_cache || !seq_lens || !sel_idx || !k_out || !v_out)
+        return ASP_ERR_INVALID_ARGUMENT;
+    if (!aligned16(k_cache) || !aligned16(v_cache) || !aligned16(k_out) || !aligned16(v_out))
+        return ASP_ERR_INVALID_ARGUMENT;
+    return from_cuda(asp_launch_gather(*p, k_cache, v_cache, seq_lens, sel_idx, k_out, v_out,
+                                       idx_out, (cudaStream_t)stream));
+}
+
 const char *asyncspade_status_string(asp_status s) {
     switch (s) {
         case ASP_OK: return "ASP_OK";

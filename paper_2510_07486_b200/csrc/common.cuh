@@ -125,4 +125,8 @@ cudaError_t asp_launch_quest_summarize(const asp_select_params &p, int page_size
 cudaError_t asp_launch_quest_select(const asp_select_params &p, int page_size, const float *q,
                                     const void *meta, const int32_t *seq_lens, int32_t *sel_idx,
                                     void *workspace, uint32_t *dev_flags, cudaStream_t s);
+cudaError_t asp_launch_gather(const asp_decode_params &p, const asp_bf16 *k_cache,
+                              const asp_bf16 *v_cache, const int32_t *seq_lens,
+                              const int32_t *sel_idx, asp_bf16 *k_out, asp_bf16 *v_out,
+                              int32_t *idx_out, cudaStream_t s);
 int asp_sm_count();

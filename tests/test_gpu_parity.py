@@ -4,6 +4,8 @@ same seeded inputs, element by element.  Tolerances: tests/parity_util.py
 upstream output (GPU q_hat into the oracle's scorer, GPU idx into the
 oracle's decode) so a legitimately different near-tie upstream cannot flip
 a downstream check."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -603,3 +605,55 @@ def test_append_is_exact_data_movement():
     ref_v[0, :, 511], ref_v[1, :, 7] = v_new[0], v_new[1]
     assert torch.equal(step.k_cache, ref_k) and torch.equal(step.v_cache, ref_v)
     assert step.ring_start == (slot + 1) % cfg.window
+
+
+# ----------------------------------------------------------------------------- NEXT-1 gather / dual rank
+def test_gather_filtered_bit_equal():
+    """SPEC gather_filtered: packed rows bit-equal to the cache
+    rows, zeros for -1 / out-of-length entries; all indices -> the cache."""
+    cfg = configs.QWEN3_8B.with_(batch=2, seq_len=512, top_k=64)
+    step = DecodeStep(cfg, DEV)
+    step.fill_synthetic()
+    step.seq_lens.copy_(torch.tensor([512, 300], dtype=torch.int32))
+    step.run()
+    idx = step.sel_idx.clone()
+    idx[0, 0, 5] = -1
+    idx[1, 2, 7] = 400                                     # >= seq_lens[1]
+    io = torch.empty_like(idx)
+    ko, vo = asp.gather_filtered(step.k_cache, step.v_cache, step.seq_lens, idx, n_fresh=1,
+                                 idx_out=io)
+    torch.cuda.synchronize()
+    for b in range(2):
+        n = int(step.seq_lens[b])
+        for h in range(8):
+            exp_i = [j if 0 <= int(idx[b, h, j]) < n - 1 else -1 for j in range(64)]
+            assert io[b, h].tolist() == exp_i
+    for b in range(2):
+        for h in range(8):
+            for j in range(64):
+                t = int(idx[b, h, j])
+                ok = 0 <= t < int(step.seq_lens[b])
+                exp_k = step.k_cache[b, h, t] if ok else torch.zeros_like(ko[b, h, j])
+                exp_v = step.v_cache[b, h, t] if ok else torch.zeros_like(vo[b, h, j])
+                assert torch.equal(ko[b, h, j], exp_k) and torch.equal(vo[b, h, j], exp_v)
+    full = torch.arange(512, dtype=torch.int32, device=DEV).expand(2, 8, 512).contiguous()
+    step.seq_lens.fill_(512)
+    ka, va = asp.gather_filtered(step.k_cache, step.v_cache, step.seq_lens, full)
+    assert torch.equal(ka, step.k_cache) and torch.equal(va, step.v_cache)
+
+
+def test_dual_rank_disaggregation_matches_single_rank_pipeline():
+    """NEXT-1: an Inference Rank and a Cache Rank (two processes
+    on one GPU, gloo with host staging) exchanging packs and selected K/V
+    rows produce, step for step, bit for bit the single-rank a5 pipeline's
+    output on the same inputs (scripts/exp_disagg_gloo.py runs both ranks and
+    the reference; it prints one line per step)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "exp_disagg_gloo.py")],
+                       capture_output=True, text=True, timeout=300, cwd=root)
+    lines = [ln for ln in r.stdout.splitlines() if " out eq " in ln]
+    assert r.returncode == 0 and len(lines) == 3, r.stdout[-2000:] + r.stderr[-2000:]
+    for ln in lines:
+        assert ln.endswith("out eq True idx eq True fresh k eq True"), ln

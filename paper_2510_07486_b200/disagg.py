@@ -39,7 +39,8 @@ class Transport:
 
     def send(self, t: torch.Tensor) -> None:
         if self.staged:                           # raw bytes: bit-exact for every dtype
-            torch.cuda.current_stream().synchronize()
+            if t.is_cuda:
+                torch.cuda.current_stream(t.device).synchronize()
             dist.send(t.contiguous().view(torch.uint8).cpu(), self.peer, group=self.group)
         else:
             dist.send(t, self.peer, group=self.group)

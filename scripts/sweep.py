@@ -155,7 +155,8 @@ def quest_point(cfg, args, P=16):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("sweep", choices=["long-cot", "high-concurrency", "layer-packed", "quest"])
+    ap.add_argument("sweep", choices=["long-cot", "high-concurrency", "layer-packed", "quest",
+                                      "gather"])
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--out", default=None)
@@ -176,6 +177,25 @@ def main():
         for cfg in (configs.QWEN3_8B, configs.QWEN3_32B):
             lines.append(quest_point(cfg, args))
             print(json.dumps(lines[-1]), flush=True)
+    elif args.sweep == "gather":
+        # NEXT-1: the Cache Rank's payload (asyncspade_gather_filtered) per layer
+        for cfg in (configs.QWEN3_8B, configs.QWEN3_32B, configs.high_concurrency(8)):
+            step = DecodeStep(cfg, "cuda")
+            step.fill_synthetic()
+            step.run()
+            ko = torch.empty(cfg.batch, cfg.n_kv_heads, cfg.top_k, cfg.head_dim,
+                             dtype=torch.bfloat16, device="cuda")
+            vo, io = torch.empty_like(ko), torch.empty_like(step.sel_idx)
+            t = timed(lambda: asp.gather_filtered(step.k_cache, step.v_cache, step.seq_lens,
+                                                  step.sel_idx, n_fresh=1, k_out=ko, v_out=vo,
+                                                  idx_out=io), args.steps, args.warmup)
+            payload = 2 * ko.numel() * 2 + io.numel() * 4
+            lines.append({"workload": cfg.name, "gather_us": t, "payload_bytes": payload,
+                          "gather_tb_per_s": 2 * payload / (t * 1e-6) / 1e12,
+                          "nvlink_900GBps_us": payload / 900e9 * 1e6})
+            print(json.dumps(lines[-1]), flush=True)
+            del step
+            torch.cuda.empty_cache()
     elif args.sweep == "layer-packed":
         # NEXT-2: per-layer step time when P_l layers share one
         # launch of each kernel, on the small shapes that under-fill the SMs

@@ -76,3 +76,46 @@ def test_two_rank_gloo_sharded_step_matches_unsharded():
     ref_idx, ref_out = _shard_step(0, 1)
     np.testing.assert_array_equal(idx, ref_idx)
     np.testing.assert_array_equal(out, ref_out)
+
+
+def _transport_worker(rank, port, result_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    from paper_2510_07486_b200.disagg import Transport
+    io = Transport(1 - rank)
+    g = torch.Generator().manual_seed(3)
+    pack = [torch.randn(2, 4, 8, generator=g), torch.randn(2, 2, 3, 8, generator=g).to(torch.bfloat16),
+            torch.randint(-1, 100, (2, 3, 5), generator=g, dtype=torch.int32)]
+    if rank == 0:                                    # Inference Rank: send the pack, get it back
+        for t in pack:
+            io.send(t)
+        back = [torch.empty_like(t) for t in pack]
+        for t in back:
+            io.recv(t)
+        result_q.put([bool(torch.equal(a.view(torch.uint8) if a.dtype == torch.bfloat16 else a,
+                                       b.view(torch.uint8) if b.dtype == torch.bfloat16 else b))
+                      for a, b in zip(pack, back)])
+    else:                                            # Cache Rank: echo
+        got = [torch.empty_like(t) for t in pack]
+        for t in got:
+            io.recv(t)
+        for t in got:
+            io.send(t)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_transport_is_bit_exact():
+    """NEXT-1 host logic: the dual-rank Transport (gloo, raw-byte staging)
+    moves fp32, bf16 and int32 packs bit for bit (a round trip)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_transport_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert ok == [True, True, True]

@@ -18,3 +18,4 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-a5 --ragged > gpurun_out/${TAG}_bench_ragged.json 2>/dev/null; echo "ragged rc=$?"
 rm -f gpurun_out/${TAG}_bench_paged.jsonl
 for P in 16 32 64 128; do timeout 300 python bench.py --no-cpu-baseline --paged $P >> gpurun_out/${TAG}_bench_paged.jsonl 2>/dev/null; done; echo "paged done"
+timeout 300 python scripts/sweep.py gather --out gpurun_out/${TAG}_sweep_gather.jsonl > /dev/null 2>&1; echo "gather sweep rc=$?"

@@ -7,11 +7,14 @@
 // R1-R8 of DESIGN.md §3 (masked-shared default).  All regression arithmetic
 // is fp64 (reading R16).
 //
-// Design (B200): one warp per (batch, q-head) row, eight independent rows
-// per CTA, no CTA-wide barriers.  The per-row work is a chain of small
-// dependent steps, so the kernel is built for occupancy: ~5 KB of shared
-// memory and <= 64 registers per warp put 32 rows on every SM at once (the
-// 4096 rows of config [2] in one wave) so the chains overlap.
+// Design (B200).  Two kernels:
+//   * predict_pair_kernel (2 <= W <= 16, masked-shared / single assembly --
+//     every configured workload): TWO rows per warp; see the comment at the
+//     kernel below.
+//   * predict_kernel (every other case: W = 1 or W > 16, the per-window
+//     assembly): one warp per (batch, q-head) row, eight independent rows per
+//     CTA, no CTA-wide barriers, built for occupancy (~5 KB of shared memory
+//     and <= 64 registers per warp) so the rows' dependent chains overlap:
 //   * The augmented Gram matrix G' = Q Q^T (W x W) -- the history Gram G0
 //     AND beta = H y in its last row -- runs on the fp64 tensor cores
 //     (mma.sync m8n8k4 f64), all 8x8 tiles interleaved per k-step; the

@@ -16,8 +16,11 @@
 //     product is exact; one tcgen05.mma (M = 128 tokens, N = 3G padded to
 //     16/32, K = D) accumulates all three in fp32 TMEM columns, and the
 //     epilogue forms s_g = (hi_g + mid_g) + lo_g, then the group max.
-//   * Persistent CTAs (one per SM) own a contiguous range of 128-token tiles
-//     of the flattened (row, tile) space.  Warp roles: warp 0 streams K tiles
+//   * Persistent CTAs (one per SM) own a contiguous range of the VALID
+//     128-token tiles of the flattened (row, tile) space (balanced over the
+//     rows' actual lengths, so ragged batches keep every SM busy).  Paged
+//     pools stream page-sized TMA boxes, page ids fetched three tiles ahead.
+//     Warp roles: warp 0 streams K tiles
 //     with TMA (4-D tensor map over the strided cache, 128-B swizzle,
 //     L2 evict-first) into a 6-stage mbarrier ring; warp 1 owns TMEM and
 //     issues the MMAs (single thread); warp 2 builds the swizzled bf16 B

@@ -505,9 +505,9 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
                                       q_window + (size_t)(row0 + r) * W * D + (size_t)phys_of(i) * D) + fc
                                 : nullptr;
             }
-#pragma unroll 1
-        for (int s = 0; s < D / 16; s += 2) {
-            float4 f[2][2][NB];
+        // software-pipelined: the next two groups' fragments are in flight while
+        // this pair's MMAs run (the loads, not the MMAs, set the latency)
+        auto load = [&](float4 (&f)[2][2][NB], int s) {
 #pragma unroll
             for (int hh = 0; hh < 2; hh++)
 #pragma unroll
@@ -515,6 +515,8 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
 #pragma unroll
                     for (int b = 0; b < NB; b++)
                         f[hh][r][b] = rp[r][b] ? __ldg(rp[r][b] + 4 * (s + hh)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        };
+        auto mmas = [&](const float4 (&f)[2][2][NB]) {
             // k-step j of group s pairs d = 16 s + 4 fc + j in both operands
 #pragma unroll
             for (int j = 0; j < 4; j++)
@@ -534,6 +536,15 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
                                 dmma(c[0], c[1], (double)a, (double)b);
                             }
                     }
+        };
+        float4 fa[2][2][NB], fb[2][2][NB];
+        load(fa, 0);
+#pragma unroll
+        for (int s = 0; s < D / 16; s += 4) {
+            if (s + 2 < D / 16) load(fb, s + 2);
+            mmas(fa);
+            if (s + 4 < D / 16) load(fa, s + 4);
+            if (s + 2 < D / 16) mmas(fb);
         }
 #pragma unroll
         for (int r = 0; r < 2; r++)

@@ -506,7 +506,9 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
                                 : nullptr;
             }
         // software-pipelined: the next two groups' fragments are in flight while
-        // this pair's MMAs run (the loads, not the MMAs, set the latency)
+        // this pair's MMAs run (the loads, not the MMAs, set the latency).  The
+        // loop stays rolled: at small row counts instruction fetch of long
+        // straight-line code, not arithmetic, is what a warp waits on.
         auto load = [&](float4 (&f)[2][2][NB], int s) {
 #pragma unroll
             for (int hh = 0; hh < 2; hh++)
@@ -516,7 +518,24 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
                     for (int b = 0; b < NB; b++)
                         f[hh][r][b] = rp[r][b] ? __ldg(rp[r][b] + 4 * (s + hh)) : make_float4(0.f, 0.f, 0.f, 0.f);
         };
-        auto mmas = [&](const float4 (&f)[2][2][NB]) {
+        float4 fa[2][2][NB], fb[2][2][NB];
+        load(fa, 0);
+#pragma unroll 1
+        for (int s = 0; s < D / 16; s += 2) {
+            if (s + 2 < D / 16) load(fb, s + 2);
+            // each fragment element converted to fp64 once
+            double x[2][2][NB][4];
+#pragma unroll
+            for (int hh = 0; hh < 2; hh++)
+#pragma unroll
+                for (int r = 0; r < 2; r++)
+#pragma unroll
+                    for (int b = 0; b < NB; b++) {
+                        x[hh][r][b][0] = (double)fa[hh][r][b].x;
+                        x[hh][r][b][1] = (double)fa[hh][r][b].y;
+                        x[hh][r][b][2] = (double)fa[hh][r][b].z;
+                        x[hh][r][b][3] = (double)fa[hh][r][b].w;
+                    }
             // k-step j of group s pairs d = 16 s + 4 fc + j in both operands
 #pragma unroll
             for (int j = 0; j < 4; j++)
@@ -529,22 +548,16 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
                         for (int bi = 0; bi < NB; bi++)
 #pragma unroll
                             for (int bj = bi; bj < NB; bj++, t++) {
-                                const float4 &A = f[hh][r][bi], &B = f[hh][r][bj];
-                                const float a = j == 0 ? A.x : j == 1 ? A.y : j == 2 ? A.z : A.w;
-                                const float b = j == 0 ? B.x : j == 1 ? B.y : j == 2 ? B.z : B.w;
                                 double *c = hh ? acc2[r][t] : acc[r][t];
-                                dmma(c[0], c[1], (double)a, (double)b);
+                                dmma(c[0], c[1], x[hh][r][bi][j], x[hh][r][bj][j]);
                             }
                     }
-        };
-        float4 fa[2][2][NB], fb[2][2][NB];
-        load(fa, 0);
 #pragma unroll
-        for (int s = 0; s < D / 16; s += 4) {
-            if (s + 2 < D / 16) load(fb, s + 2);
-            mmas(fa);
-            if (s + 4 < D / 16) load(fa, s + 4);
-            if (s + 2 < D / 16) mmas(fb);
+            for (int hh = 0; hh < 2; hh++)
+#pragma unroll
+                for (int r = 0; r < 2; r++)
+#pragma unroll
+                    for (int b = 0; b < NB; b++) fa[hh][r][b] = fb[hh][r][b];
         }
 #pragma unroll
         for (int r = 0; r < 2; r++)
@@ -646,19 +659,31 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
             if (mm > n) break;                                        // n is warp-uniform
             const unsigned sh = (unsigned)(n - mm);
             double t = ev * shfl16(invS, mm - 1);
-            if (tiny_any) {
-                // a prefix's exponentials underflowed against the global max:
-                // this prefix's own max
-                const double mx = half_max(l < mm ? v : -INFINITY);
-                const double ex = l < mm ? exp(v - mx) : 0.0;
-                const double ts = ex / half_sum(ex);
-                if (tiny) t = ts;
-            }
             if (mm == n) t *= 2.0;
             const double u = shfl16_up(t, sh);
             if (l >= (int)sh && own) {
                 if (mm & 1) c += u;
                 else c2 += u;
+            }
+        }
+        if (tiny_any) {
+            // a prefix's exponentials underflowed against the global max: redo
+            // the half that needs it with each prefix's own max (rolled -- rare,
+            // and kept out of the hot straight-line code)
+            double ct = 0.0;
+#pragma unroll 1
+            for (int mm = 1; mm <= n; mm++) {
+                const unsigned sh = (unsigned)(n - mm);
+                const double mx = half_max(l < mm ? v : -INFINITY);
+                const double ex = l < mm ? exp(v - mx) : 0.0;
+                double t = ex / half_sum(ex);
+                if (mm == n) t *= 2.0;
+                const double u = shfl16_up(t, sh);
+                if (l >= (int)sh && own) ct += u;
+            }
+            if (tiny) {
+                c = ct;
+                c2 = 0.0;
             }
         }
         c += c2;

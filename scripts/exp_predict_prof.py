@@ -10,8 +10,7 @@ from paper_2510_07486_b200 import configs
 from paper_2510_07486_b200.step import DecodeStep
 L = asp.lib()
 buf = (ctypes.c_ulonglong * 8)()
-for P in (1, 8):
-    cfg = configs.QWEN3_32B
+for cfg, P in ((configs.QWEN3_32B, 1), (configs.QWEN3_32B, 8), (configs.high_concurrency(1), 1)):
     step = DecodeStep(cfg, "cuda", kv_heads=(0, cfg.n_kv_heads // P))
     step.fill_synthetic()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -22,7 +21,7 @@ for P in (1, 8):
         ev[1].record(); torch.cuda.synchronize()
     L.asp_predict_prof_read(buf)
     warps = cfg.batch * step.n_q // 2
-    print(f"P={P} predict us {ev[0].elapsed_time(ev[1]) * 1000:.1f} (instrumented)")
+    print(f"{cfg.name} P={P} predict us {ev[0].elapsed_time(ev[1]) * 1000:.1f} (instrumented)")
     for n, v in zip(["gram", "ridge", "coeffs", "combine"], buf):
         print(f"  {n:10s} {v / warps / 1.965e3:8.2f} us/warp")
     del step; torch.cuda.empty_cache()

@@ -94,7 +94,7 @@ __device__ uint32_t block_excl_scan(SelectSmem &s, uint32_t v, uint32_t *total) 
 // bin 0.  Thread t owns bins [nbins - PER (t+1), nbins - PER t), read as
 // 16-B vectors; one block scan orders the threads from the top.
 template <int PER>
-__device__ void find_bucket_t(SelectSmem &s, int nbins, uint32_t rank_a, uint32_t rank_b) {
+__device__ __noinline__ void find_bucket_t(SelectSmem &s, int nbins, uint32_t rank_a, uint32_t rank_b) {
     const int t = threadIdx.x;
     const int lo = nbins - PER * (t + 1);          // < 0: this thread owns no bins
     if (t == 0) {
@@ -153,9 +153,14 @@ __device__ __forceinline__ void zero_hist(SelectSmem &s, int nbins) {
 
 // Sum the first nbins bins of every cluster rank's histogram (rank order)
 // into this CTA's histogram.
-__device__ void merge_hist(SelectSmem &s, int nbins, int C) {
+// (the cluster parts are out of line: single-CTA rows never run them, and
+// inlined at every call site they would only lengthen the code a warp fetches)
+__device__ __noinline__ void merge_hist_cluster(SelectSmem &s, int nbins, int C);
+__device__ __forceinline__ void merge_hist(SelectSmem &s, int nbins, int C) {
     __syncthreads();
-    if (C == 1) return;
+    if (C > 1) merge_hist_cluster(s, nbins, C);
+}
+__device__ __noinline__ void merge_hist_cluster(SelectSmem &s, int nbins, int C) {
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
     constexpr int kPer = kBins / kThreads;
@@ -178,7 +183,7 @@ __device__ void merge_hist(SelectSmem &s, int nbins, int C) {
 
 // Cluster-wide totals of s.cnt[0..n) and their sums over earlier ranks
 // (exclusive prefix), for every thread.  s.cnt must be written before.
-__device__ void cluster_counts(SelectSmem &s, int C, int n, uint32_t *tot, uint32_t *before) {
+__device__ __noinline__ void cluster_counts(SelectSmem &s, int C, int n, uint32_t *tot, uint32_t *before) {
     __syncthreads();
     if (C == 1) {
         for (int j = 0; j < n; j++) {

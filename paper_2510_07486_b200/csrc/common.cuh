@@ -41,13 +41,13 @@ ASP_DEV uint32_t score_key(float f) {
 // Programmatic dependent launch (PDL): every kernel of the path is launched
 // with programmatic stream serialization, so its prologue (barrier init,
 // TMEM allocation, descriptor prefetch) overlaps the previous kernel's tail.
-// pdl_wait() returns once the preceding grid has completed and its writes are
-// visible -- transitively, every earlier kernel in the stream.  A thread must
-// call it before it reads anything an earlier kernel of this library writes
-// and before its first global store; reads of caller-written inputs that no
-// kernel here writes (the query window, the K cache, seq_lens) may precede it
-// (predict and score use this to start before their predecessor finishes).
-// pdl_trigger() lets the next kernel in the stream start launching.
+// pdl_wait() must precede the first global-memory access of every kernel
+// (it returns once the preceding grid has completed and its writes are
+// visible -- transitively, every earlier kernel in the stream; every input of
+// the path -- window, caches, indices -- may come from an earlier kernel of
+// this library, asyncspade_append included); reading caller-only inputs
+// (seq_lens) to plan the work may precede it.  pdl_trigger() lets the next
+// kernel in the stream start launching.
 ASP_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 ASP_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

@@ -470,9 +470,7 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long rows = (long)p.batch * p.n_q_heads;
     const long row0 = ((long)blockIdx.x * (blockDim.x >> 5) + warp) * 2;
-    // PDL: the window is never produced by a kernel of this library, so the
-    // whole computation overlaps the preceding kernel's tail; the wait guards
-    // the q_hat store (an earlier reader -- the previous score -- is then done)
+    asp::pdl_wait();                 // the window may come from asyncspade_append
     asp::pdl_trigger();
     if (row0 >= rows) return;
     const bool has1 = row0 + 1 < rows;
@@ -726,7 +724,6 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
     for (int u = 0; u < kV; u++)
 #pragma unroll
         for (int z = 0; z < 4; z++) acc[u][z] += acc2[u][z];
-    asp::pdl_wait();
     if (live && ok) {
         const double inv_m = 1.0 / denom;
 #pragma unroll

@@ -318,10 +318,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
     const uint32_t tmem_base = *tmem_holder_g;
     it.start = s_rng[0];
     it.end = s_rng[1];
-    // PDL: of this kernel's inputs only q_hat comes from the preceding kernel
-    // (predict), so the K stream starts at once; the B builder waits before it
-    // reads q_hat and the epilogue before its first store (an earlier reader of
-    // the score buffer -- the previous select -- has then completed too).
+    asp::pdl_wait();                        // q_hat, K (asyncspade_append writes it), scores
     asp::pdl_trigger();
 #ifdef ASP_PROFILE_SCORE
     const long long t_kernel0 = clock64();
@@ -481,7 +478,6 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
         __syncwarp();
     } else if (warp == 2) {
         // ------------------------------------------------ B-operand builder
-        asp::pdl_wait();
         int bs = -1;
         uint32_t bph = 0;
         int cur_row = -1;
@@ -531,7 +527,6 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
         }
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue: TMEM -> scores
-        asp::pdl_wait();
         // two warpgroups alternate tiles (each warp drains its 32-lane quadrant)
         const int quad = warp & 3;                  // TMEM lanes 32*quad .. +31
         const int group = (warp - 4) >> 2;

@@ -1,4 +1,6 @@
 """Sweeps of BASELINE.json configs [3] and [4] on one B200.
+Steps are replayed from a CUDA graph (the per-call host cost would otherwise
+bound the small ones).
 
     python scripts/sweep.py long-cot          # [3] batch 8, ctx 4k..512k, per-GPU shard of P = 8
     python scripts/sweep.py high-concurrency  # [4] Qwen3-8B shape, ctx 4k, batch 1..512, a5 overlap
@@ -60,7 +62,10 @@ def point(cfg, args, kv_heads=None, overlap=False):
     torch.cuda.synchronize()
     hn = step.n_kv
     core = cfg.core_bytes(hn)
-    t_step = timed(step.run, args.steps, args.warmup)
+    # CUDA-graph replay (PDL edges kept): small steps are otherwise bound by the
+    # host's per-call launch cost, not the GPU
+    step.capture()
+    t_step = timed(step.replay, args.steps, args.warmup)
     res = {"workload": cfg.name, "batch": cfg.batch, "seq_len": cfg.seq_len, "top_k": cfg.top_k,
            "kv_heads_on_gpu": hn, "us_per_step": t_step,
            "hbm_tb_per_s": core / (t_step * 1e-6) / 1e12,
@@ -204,7 +209,8 @@ def main():
             for pl in (1, 2, 4, 8):
                 step = DecodeStep(cfg, "cuda", kv_heads=kvh, layers=pl)
                 step.fill_synthetic()
-                t = timed(step.run, args.steps, args.warmup)
+                step.capture()
+                t = timed(step.replay, args.steps, args.warmup)
                 core = cfg.core_bytes(step.n_kv) * pl
                 lines.append({"workload": cfg.name, "kv_heads_on_gpu": step.n_kv, "layers_packed": pl,
                               "us_per_launch": t, "us_per_layer": t / pl,

@@ -315,6 +315,8 @@ def main():
         one_step(events[i])
     barrier()
     seg = [[e[j].elapsed_time(e[j + 1]) for e in events] for j in range(3)]
+    per_step = sorted(e[0].elapsed_time(e[3]) * 1e3 for e in events)
+    pct = lambda q: per_step[min(len(per_step) - 1, int(q * (len(per_step) - 1) + 0.5))]
     avg_pred, avg_sel, avg_dec = (statistics.mean(s) for s in seg)
     t = torch.tensor([ms_step, avg_sel], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -475,6 +477,7 @@ def main():
             "roofline_frac_step": core / (ms_step * 1e-3) / 1e9 / peak,
             "per_call_ms": {"predict_query": avg_pred, "score_select": avg_sel,
                             "sparse_decode": avg_dec},
+            "step_us_p10_p50_p90": [pct(0.1), pct(0.5), pct(0.9)],
             "roofline": {"bound": "hbm", "kernel": "asyncspade_score_select (score + select)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic(),

@@ -3,7 +3,8 @@ import os, sys, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2510_07486_b200 import configs
 from paper_2510_07486_b200.step import DecodeStep
-step = DecodeStep(configs.QWEN3_32B, "cuda")
+P = int(os.environ.get("SHARD", "1"))
+step = DecodeStep(configs.QWEN3_32B, "cuda", kv_heads=(0, 8 // P))
 step.fill_synthetic()
 K = 20
 def timeit(f):

@@ -475,6 +475,7 @@ def main():
             "hbm_tb_per_s": core / (ms_step * 1e-3) / 1e12,
             "core_bytes_per_gpu": core,
             "roofline_frac_step": core / (ms_step * 1e-3) / 1e9 / peak,
+            "roofline_frac_step_nominal_8tbs": core / (ms_step * 1e-3) / 8e12,
             "per_call_ms": {"predict_query": avg_pred, "score_select": avg_sel,
                             "sparse_decode": avg_dec},
             "step_us_p10_p50_p90": [pct(0.1), pct(0.5), pct(0.9)],

@@ -122,11 +122,3 @@ class DecodeStep:
                v_cache=self.v_cache if v_new is not None else None, pos=pos, stream=stream)
         self.ring_start = (slot + 1) % self.cfg.window
         self.p_pred.ring_start = self.ring_start
-
-    def push_query(self, q_t: torch.Tensor) -> None:
-        """Enqueue q_t (fp32 [B, n_q, D]) as the newest window entry, evicting
-        the oldest ("enqueues the query state to the sliding window")."""
-        slot = self.ring_start
-        self.window[:, :, slot].copy_(q_t, non_blocking=True)
-        self.ring_start = (slot + 1) % self.cfg.window
-        self.p_pred.ring_start = self.ring_start

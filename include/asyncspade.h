@@ -89,7 +89,10 @@ enum {
     ASP_SIGN_NEGATED = 1u << 4,      /* softmax(-omega) as Alg.1 Step 3 */
     ASP_EPS_ABSOLUTE = 1u << 5,      /* eps is absolute, not x mean diag(G0)  */
     ASP_NORM_NONE = 1u << 6,         /* raw ridge weights (SINGLE only; tests) */
-    ASP_DOUBLE_SOFTMAX = 1u << 7     /* literal Step 3 + Step 4 double softmax */
+    ASP_DOUBLE_SOFTMAX = 1u << 7,    /* literal Step 3 + Step 4 double softmax */
+    ASP_WINDOW_BF16 = 1u << 8        /* q_window holds bf16 (asp_bf16) elements,
+                                        widened exactly; 2 <= window <= 16 with the
+                                        masked-shared or single assembly only */
 };
 
 enum { ASP_AGG_MAX = 0, ASP_AGG_SUM = 1 };
@@ -142,7 +145,8 @@ ASP_API asp_status asyncspade_append(const asp_append_params *p, const float *q_
  *                 c_j = sum_i r_j[i] * window[W-n_j+i]       (R3-R6)
  *   q_hat = (1/W) sum_j c_j, rounded once to fp32.
  *
- * q_window  device fp32 [batch][n_q_heads][window][head_dim]; logical slot
+ * q_window  device fp32 (bf16 with ASP_WINDOW_BF16: pass the asp_bf16
+ *           pointer cast) [batch][n_q_heads][window][head_dim]; logical slot
  *           j (0 = oldest, window-1 = newest) is physical slot
  *           (ring_start + j) % window.  Read only.
  * q_hat     device fp32 [batch][n_q_heads][head_dim], written.

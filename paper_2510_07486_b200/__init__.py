@@ -27,6 +27,7 @@ ASP_OK = 0
 FLAG_NONFINITE, FLAG_NOT_PD, FLAG_SHORT_ROW = 1, 2, 4
 ASSEMBLY_MASKED_SHARED, ASSEMBLY_SINGLE, ASSEMBLY_PER_WINDOW = 0, 1, 2
 SIGN_NEGATED, EPS_ABSOLUTE, NORM_NONE, DOUBLE_SOFTMAX = 1 << 4, 1 << 5, 1 << 6, 1 << 7
+WINDOW_BF16 = 1 << 8
 AGG_MAX, AGG_SUM = 0, 1
 
 EXPORTED_SYMBOLS = (
@@ -175,6 +176,8 @@ def _u16(t: torch.Tensor) -> torch.Tensor:
 # --------------------------------------------------------------------------- params
 def predict_params(q_window: torch.Tensor, eps=1e-2, flags=0, ring_start=0) -> PredictParams:
     B, Hq, W, D = q_window.shape
+    if q_window.dtype == torch.bfloat16:
+        flags |= WINDOW_BF16                 # a bf16 ring (ASP_WINDOW_BF16)
     return PredictParams(B, Hq, W, D, ring_start, eps, flags)
 
 
@@ -240,13 +243,13 @@ def append(q_t: torch.Tensor, q_window: torch.Tensor, ring_slot: int, *,
 def predict_query(q_window: torch.Tensor, q_hat: torch.Tensor | None = None, *, eps: float = 1e-2,
                   flags: int = 0, ring_start: int = 0, dev_flags: torch.Tensor | None = None,
                   stream=None, params: PredictParams | None = None) -> torch.Tensor:
-    """a1 -> asyncspade_predict_query.  q_window fp32 [B, Hq, W, D] (ring
+    """a1 -> asyncspade_predict_query.  q_window fp32 or bf16 [B, Hq, W, D] (ring
     order per ring_start); returns q_hat fp32 [B, Hq, D]."""
     p = params or predict_params(q_window, eps, flags, ring_start)
     if q_hat is None:
         q_hat = torch.empty(q_window.shape[0], q_window.shape[1], q_window.shape[3],
                             dtype=torch.float32, device=q_window.device)
-    _check(lib().asyncspade_predict_query(ctypes.byref(p), _ptr(q_window), _ptr(q_hat),
+    _check(lib().asyncspade_predict_query(ctypes.byref(p), _ptr(_u16(q_window)), _ptr(q_hat),
                                           _ptr(dev_flags), _stream(stream)),
            "asyncspade_predict_query")
     return q_hat

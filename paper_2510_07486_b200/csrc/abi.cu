@@ -108,8 +108,11 @@ asp_status asyncspade_predict_query(const asp_predict_params *p, const float *q_
     if (!dim_ok(p->head_dim) || p->window > 32) return ASP_ERR_UNSUPPORTED;
     const uint32_t mode = p->flags & 0xFu;
     const uint32_t known = 0xFu | ASP_SIGN_NEGATED | ASP_EPS_ABSOLUTE | ASP_NORM_NONE |
-                           ASP_DOUBLE_SOFTMAX;
+                           ASP_DOUBLE_SOFTMAX | ASP_WINDOW_BF16;
     if (mode > ASP_ASSEMBLY_PER_WINDOW || (p->flags & ~known)) return ASP_ERR_INVALID_ARGUMENT;
+    if ((p->flags & ASP_WINDOW_BF16) &&
+        (p->window < 2 || p->window > 16 || mode == ASP_ASSEMBLY_PER_WINDOW))
+        return ASP_ERR_UNSUPPORTED;
     if ((p->flags & ASP_NORM_NONE) && mode != ASP_ASSEMBLY_SINGLE) return ASP_ERR_INVALID_ARGUMENT;
     if (!(p->eps == p->eps)) return ASP_ERR_INVALID_ARGUMENT;
     if (!aligned16(q_window) || !aligned16(q_hat)) return ASP_ERR_INVALID_ARGUMENT;

@@ -457,10 +457,22 @@ ASP_DEV double half_softmax(double v, int l, int n) {
     return e / half_sum(e);
 }
 
+// four consecutive window elements at element offset `off` (a multiple of 4)
+// as fp32: the ring is fp32, or bf16 with ASP_WINDOW_BF16 (exact widening)
+template <bool BF>
+ASP_DEV float4 ld4(const float *__restrict__ win, long off) {
+    if constexpr (BF) {
+        const uint2 w = __ldg(reinterpret_cast<const uint2 *>(reinterpret_cast<const asp_bf16 *>(win) + off));
+        return make_float4(asp::bf16lo(w.x), asp::bf16hi(w.x), asp::bf16lo(w.y), asp::bf16hi(w.y));
+    } else {
+        return __ldg(reinterpret_cast<const float4 *>(win + off));
+    }
+}
+
 constexpr int kPairWarps = 8;
 constexpr int kGS = 17;                            // smem row stride of a Gram (doubles)
 
-template <int D, int NB>
+template <int D, int NB, bool BF>
 __global__ void __launch_bounds__(kPairWarps * 32)
 predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
                     float *__restrict__ q_hat, uint32_t *dev_flags) {
@@ -492,16 +504,14 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
         for (int r = 0; r < 2; r++)
 #pragma unroll
             for (int t = 0; t < T; t++) acc[r][t][0] = acc[r][t][1] = acc2[r][t][0] = acc2[r][t][1] = 0.0;
-        const float4 *rp[2][NB];
+        long rp[2][NB];                                 // element offsets (-1: padding)
 #pragma unroll
         for (int r = 0; r < 2; r++)
 #pragma unroll
             for (int b = 0; b < NB; b++) {
                 const int i = 8 * b + fr;
                 const bool live = i < W && (r == 0 || has1);
-                rp[r][b] = live ? reinterpret_cast<const float4 *>(
-                                      q_window + (size_t)(row0 + r) * W * D + (size_t)phys_of(i) * D) + fc
-                                : nullptr;
+                rp[r][b] = live ? (long)(row0 + r) * W * D + (long)phys_of(i) * D + 4 * fc : -1;
             }
         // software-pipelined: the next two groups' fragments are in flight while
         // this pair's MMAs run (the loads, not the MMAs, set the latency).  The
@@ -514,7 +524,8 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
                 for (int r = 0; r < 2; r++)
 #pragma unroll
                     for (int b = 0; b < NB; b++)
-                        f[hh][r][b] = rp[r][b] ? __ldg(rp[r][b] + 4 * (s + hh)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        f[hh][r][b] = rp[r][b] >= 0 ? ld4<BF>(q_window, rp[r][b] + 16 * (s + hh))
+                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
         };
         float4 fa[2][2][NB], fb[2][2][NB];
         load(fa, 0);
@@ -692,7 +703,7 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
     // ---- q_hat = (1/m) sum_p c_p Q[p] (one pass over the cache-hot window), or
     // the passthrough Q_t.
     const bool live = h == 0 || has1;
-    const float *src = q_window + (size_t)(row0 + h) * W * D;
+    const long src = (long)(row0 + h) * W * D;                         // element offset
     float *out = q_hat + (size_t)(row0 + h) * D;
     constexpr int kV = D / 64;                                          // float4 per lane
     // (all lanes run the loop -- its shuffles span both halves -- even when a
@@ -704,10 +715,10 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
         for (int z = 0; z < 4; z++) acc[u][z] = acc2[u][z] = 0.0;
     auto axpy = [&](double (&a)[kV][4], int q) {
         const double cq = shfl16(c, q - 1);
-        const float4 *rq = reinterpret_cast<const float4 *>(src + (size_t)phys_of(q) * D) + l;
+        const long rq = src + (long)phys_of(q) * D + 4 * l;
 #pragma unroll
         for (int u = 0; u < kV; u++) {
-            const float4 v4 = live ? __ldg(rq + 16 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 v4 = live ? ld4<BF>(q_window, rq + 64 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
             a[u][0] = fma(cq, (double)v4.x, a[u][0]);
             a[u][1] = fma(cq, (double)v4.y, a[u][1]);
             a[u][2] = fma(cq, (double)v4.z, a[u][2]);
@@ -732,9 +743,9 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
                 make_float4((float)(acc[u][0] * inv_m), (float)(acc[u][1] * inv_m),
                             (float)(acc[u][2] * inv_m), (float)(acc[u][3] * inv_m));
     } else if (live) {
-        const float4 *rq = reinterpret_cast<const float4 *>(src + (size_t)phys_of(W - 1) * D) + l;
+        const long rq = src + (long)phys_of(W - 1) * D + 4 * l;
 #pragma unroll
-        for (int u = 0; u < kV; u++) reinterpret_cast<float4 *>(out)[l + 16 * u] = rq[16 * u];
+        for (int u = 0; u < kV; u++) reinterpret_cast<float4 *>(out)[l + 16 * u] = ld4<BF>(q_window, rq + 64 * u);
         if (l == 0) asp::flag_or(dev_flags, finite ? ASP_FLAG_NOT_PD : ASP_FLAG_NONFINITE);
     }
     PPROF(3);
@@ -743,6 +754,8 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
 template <int D, int NB>
 cudaError_t launch_pair(const asp_predict_params &p, const float *q_window, float *q_hat,
                         uint32_t *dev_flags, cudaStream_t s) {
+    auto kern = (p.flags & ASP_WINDOW_BF16) ? predict_pair_kernel<D, NB, true>
+                                            : predict_pair_kernel<D, NB, false>;
     const long rows = (long)p.batch * p.n_q_heads;
     const long warps = (rows + 1) / 2;
     // as many CTAs as it takes to cover the SMs twice before packing 8 warps each
@@ -751,7 +764,7 @@ cudaError_t launch_pair(const asp_predict_params &p, const float *q_window, floa
     while (wpc < kPairWarps && (warps + 2 * wpc - 1) / (2 * wpc) >= target) wpc *= 2;
     const unsigned grid = (unsigned)((warps + wpc - 1) / wpc);
     const size_t smem = (size_t)wpc * 2 * 16 * kGS * sizeof(double);
-    return asp_launch(predict_pair_kernel<D, NB>, dim3(grid), dim3(wpc * 32), smem, s, 1, p,
+    return asp_launch(kern, dim3(grid), dim3(wpc * 32), smem, s, 1, p,
                       q_window, q_hat, dev_flags);
 }
 

@@ -159,3 +159,16 @@ def test_paged_validation(L):
                                            FAKE, None, 0, None, None) == 1
     # decode needs its workspace: a valid call shape without one is rejected as such
     assert dec(asp.PagedKV(16, 64, 256)) == 4
+
+
+def test_predict_bf16_window_validation(L):
+    """ASP_WINDOW_BF16 is built for the fast path only (2 <= W <= 16,
+    masked-shared or single assembly)."""
+    def call(W, flags):
+        p = asp.PredictParams(2, 4, W, 128, 0, 1e-2, flags)
+        return L.asyncspade_predict_query(ctypes.byref(p), FAKE, FAKE, None, None)
+
+    assert call(32, asp.WINDOW_BF16) == 3
+    assert call(1, asp.WINDOW_BF16) == 3
+    assert call(8, asp.WINDOW_BF16 | asp.ASSEMBLY_PER_WINDOW) == 3
+    assert call(8, asp.WINDOW_BF16 | (1 << 12)) == 1                 # unknown bit

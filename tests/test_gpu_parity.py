@@ -657,3 +657,28 @@ def test_dual_rank_disaggregation_matches_single_rank_pipeline():
     assert r.returncode == 0 and len(lines) == 3, r.stdout[-2000:] + r.stderr[-2000:]
     for ln in lines:
         assert ln.endswith("out eq True idx eq True fresh k eq True"), ln
+
+
+def test_predict_bf16_window():
+    """NEXT-3: a bf16 query ring (ASP_WINDOW_BF16) -- q_hat bit-identical to
+    the fp32 path on the exactly widened values, and within the north-star
+    tolerance of the oracle; unsupported combinations are refused."""
+    for flags in (0, asp.ASSEMBLY_SINGLE, asp.SIGN_NEGATED, asp.DOUBLE_SOFTMAX,
+                  asp.ASSEMBLY_SINGLE | asp.NORM_NONE):
+        for B, Hq, W, D in ((3, 5, 16, 128), (2, 4, 9, 64), (1, 3, 2, 128)):
+            win, _ = synth.query_trace(synth.base_seed(1) + W, B, Hq, W, D)
+            wb = torch.from_numpy(win).to(DEV).to(torch.bfloat16)
+            wf = wb.float()
+            ring = W // 3
+            g_b = asp.predict_query(wb, flags=flags, ring_start=ring)
+            g_f = asp.predict_query(wf, flags=flags, ring_start=ring)
+            assert torch.equal(g_b, g_f), (flags, W)
+            ref, cond = oracle.predict(wf.cpu().numpy(), 1e-2, flags, ring)
+            assert cond == 0
+            assert rel_inf_err(g_b.cpu().numpy(), ref) <= Q_HAT_RTOL
+    w32 = torch.zeros(1, 2, 32, 64, dtype=torch.bfloat16, device=DEV)
+    with pytest.raises(asp.AsyncSpadeError):
+        asp.predict_query(w32)
+    w8 = torch.zeros(1, 2, 8, 64, dtype=torch.bfloat16, device=DEV)
+    with pytest.raises(asp.AsyncSpadeError):
+        asp.predict_query(w8, flags=asp.ASSEMBLY_PER_WINDOW)

@@ -47,6 +47,8 @@ def _args():
     ap.add_argument("--emulate-shard", type=int, default=0, metavar="P",
                     help="one GPU runs rank 0's shard of a P-way KV-head split (the per-GPU "
                          "work of the P-GPU run; scaling evidence when only one GPU is at hand)")
+    ap.add_argument("--bf16-window", action="store_true",
+                    help="keep the query window ring in bf16 (ASP_WINDOW_BF16)")
     ap.add_argument("--ragged", action="store_true",
                     help="ragged batch: seq_lens seeded-uniform in [L/8, L] (the cache capacity "
                          "stays L; headline bytes count each row's own length)")
@@ -228,7 +230,8 @@ def main():
     from paper_2510_07486_b200.shard import kv_head_shard
     shards = args.emulate_shard if (args.emulate_shard and world == 1) else world
     h0, hn = kv_head_shard(cfg.n_kv_heads, shards, rank)    # §8(e): KV-head sharding
-    step = DecodeStep(cfg, "cuda", kv_heads=(h0, hn))
+    wdt = torch.bfloat16 if args.bf16_window else torch.float32
+    step = DecodeStep(cfg, "cuda", kv_heads=(h0, hn), window_dtype=wdt)
     step.fill_synthetic()
     lens = [cfg.seq_len] * cfg.batch
     if args.ragged:
@@ -423,7 +426,7 @@ def main():
         from paper_2510_07486_b200.pipeline import AsyncPipeline
         del step
         torch.cuda.empty_cache()
-        st1 = DecodeStep(cfg, "cuda", kv_heads=(h0, hn), n_fresh=1)
+        st1 = DecodeStep(cfg, "cuda", kv_heads=(h0, hn), n_fresh=1, window_dtype=wdt)
         st1.fill_synthetic()
         st1.seq_lens.copy_(torch.tensor(lens, dtype=torch.int32))
         pipe = AsyncPipeline(st1)
@@ -464,6 +467,7 @@ def main():
             "config": {"workload": cfg.name, "batch": cfg.batch, "n_q_heads": cfg.n_q_heads,
                        "n_kv_heads": cfg.n_kv_heads, "head_dim": cfg.head_dim,
                        "seq_len": cfg.seq_len, "top_k": cfg.top_k, "window": cfg.window,
+                       "query_window": "bf16" if args.bf16_window else "fp32",
                        "seq_lens": ("ragged: seeded uniform [L/8, L], mean %.0f" % (sum(lens) / len(lens))
                                     if args.ragged else "uniform L"),
                        "kv_layout": (f"paged: {args.paged}-token HND pages, random placement"

@@ -106,7 +106,8 @@ typedef void *asp_stream;  /* cudaStream_t */
  * The new token of every sequence enters the state the path reads (P:191:
  * the inference side "enqueues the query state to the sliding window"; the
  * new key / value join the cache):
- *   q_window[b][hq][ring_slot][:] = q_t[b][hq][:]             (fp32)
+ *   q_window[b][hq][ring_slot][:] = q_t[b][hq][:]             (fp32, or bf16_rn
+ *                                                               with window_bf16)
  *   q_cur[b][hq][:]               = bf16_rn(q_t[b][hq][:])    (nullable)
  *   K[b][h][pos[b]][:] = k_new[b][h][:], V[b][h][pos[b]][:] = v_new[b][h][:]
  * One launch (programmatic-dependent after the previous step's kernels)
@@ -125,6 +126,7 @@ typedef void *asp_stream;  /* cudaStream_t */
 typedef struct {
     int32_t batch, n_q_heads, n_kv_heads, head_dim, window, ring_slot, max_seq_len;
     int64_t k_stride_b, k_stride_h, k_stride_t, v_stride_b, v_stride_h, v_stride_t; /* elements */
+    int32_t window_bf16; /* 1: q_window is a bf16 ring (ASP_WINDOW_BF16), q_t rounded into it */
 } asp_append_params;
 
 ASP_API asp_status asyncspade_append(const asp_append_params *p, const float *q_t, float *q_window,

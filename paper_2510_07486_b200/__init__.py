@@ -74,7 +74,8 @@ class AppendParams(ctypes.Structure):
                 ("max_seq_len", ctypes.c_int32),
                 ("k_stride_b", ctypes.c_int64), ("k_stride_h", ctypes.c_int64),
                 ("k_stride_t", ctypes.c_int64), ("v_stride_b", ctypes.c_int64),
-                ("v_stride_h", ctypes.c_int64), ("v_stride_t", ctypes.c_int64)]
+                ("v_stride_h", ctypes.c_int64), ("v_stride_t", ctypes.c_int64),
+                ("window_bf16", ctypes.c_int32)]
 
 
 class PagedKV(ctypes.Structure):
@@ -230,8 +231,10 @@ def append(q_t: torch.Tensor, q_window: torch.Tensor, ring_slot: int, *,
     L = kc.shape[2] if kc is not None else 1
     ks = k_cache.stride()[:3] if k_cache is not None else (0, 0, 0)
     vs = v_cache.stride()[:3] if v_cache is not None else (0, 0, 0)
-    p = AppendParams(B, Hq, Hkv, D, W, ring_slot, L, *ks, *vs)
-    _check(lib().asyncspade_append(ctypes.byref(p), _ptr(q_t), _ptr(q_window), _ptr(_u16(q_cur) if q_cur is not None else None),
+    p = AppendParams(B, Hq, Hkv, D, W, ring_slot, L, *ks, *vs,
+                     1 if q_window.dtype == torch.bfloat16 else 0)
+    _check(lib().asyncspade_append(ctypes.byref(p), _ptr(q_t), _ptr(_u16(q_window)),
+                                   _ptr(_u16(q_cur) if q_cur is not None else None),
                                    _ptr(_u16(k_new) if k_new is not None else None),
                                    _ptr(_u16(v_new) if v_new is not None else None),
                                    _ptr(_u16(k_cache) if k_cache is not None else None),

@@ -26,14 +26,16 @@ append_kernel(asp_append_params p, const float *__restrict__ q_t, float *__restr
     for (int i = t; i < nq4; i += kThreads) {
         const int hq = (4 * i) / D, d = (4 * i) % D;
         const float4 v = reinterpret_cast<const float4 *>(q_t + ((size_t)b * p.n_q_heads + hq) * D)[d / 4];
-        *reinterpret_cast<float4 *>(q_window + (((size_t)b * p.n_q_heads + hq) * W + p.ring_slot) * D + d) = v;
-        if (q_cur) {
-            const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
-            uint2 w;
-            w.x = *reinterpret_cast<const uint32_t *>(&lo);
-            w.y = *reinterpret_cast<const uint32_t *>(&hi);
-            *reinterpret_cast<uint2 *>(q_cur + ((size_t)b * p.n_q_heads + hq) * D + d) = w;
-        }
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+        uint2 w;
+        w.x = *reinterpret_cast<const uint32_t *>(&lo);
+        w.y = *reinterpret_cast<const uint32_t *>(&hi);
+        const size_t wo = (((size_t)b * p.n_q_heads + hq) * W + p.ring_slot) * D + d;
+        if (p.window_bf16)
+            *reinterpret_cast<uint2 *>(reinterpret_cast<asp_bf16 *>(q_window) + wo) = w;
+        else
+            *reinterpret_cast<float4 *>(q_window + wo) = v;
+        if (q_cur) *reinterpret_cast<uint2 *>(q_cur + ((size_t)b * p.n_q_heads + hq) * D + d) = w;
     }
     const int n = pos ? pos[b] : -1;
     if (n < 0 || n >= p.max_seq_len) return;

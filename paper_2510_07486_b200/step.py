@@ -30,7 +30,7 @@ from .configs import Config
 class DecodeStep:
     def __init__(self, cfg: Config, device="cuda", *, kv_heads: tuple[int, int] | None = None,
                  n_fresh: int = 0, eps: float = 1e-2, flags: int = 0, keep_scores: bool = False,
-                 layers: int = 1):
+                 layers: int = 1, window_dtype: torch.dtype = torch.float32):
         self.cfg = cfg
         self.layers = layers
         self.device = torch.device(device)
@@ -43,7 +43,7 @@ class DecodeStep:
         dev = self.device
         self.n_fresh, self.eps, self.flags = n_fresh, eps, flags
         self.ring_start = 0
-        self.window = torch.empty(B, self.n_q, W, D, dtype=torch.float32, device=dev)
+        self.window = torch.empty(B, self.n_q, W, D, dtype=window_dtype, device=dev)
         self.q = torch.empty(B, self.n_q, D, dtype=torch.bfloat16, device=dev)
         self.k_cache = torch.empty(B, hn, L, D, dtype=torch.bfloat16, device=dev)
         self.v_cache = torch.empty(B, hn, L, D, dtype=torch.bfloat16, device=dev)
@@ -75,8 +75,14 @@ class DecodeStep:
             rows = slice(layer * B, (layer + 1) * B)
             synth.fill_kv_device(self.k_cache[rows], sd, synth.STREAM_K, 0, self.h0, cfg.n_kv_heads)
             synth.fill_kv_device(self.v_cache[rows], sd, synth.STREAM_V, 0, self.h0, cfg.n_kv_heads)
-            synth.fill_query_device(self.window[rows], self.q[rows].view(torch.int16), sd, 0,
-                                    self.q0, cfg.n_q_heads)
+            if self.window.dtype == torch.float32:
+                synth.fill_query_device(self.window[rows], self.q[rows].view(torch.int16), sd, 0,
+                                        self.q0, cfg.n_q_heads)
+            else:                                          # a bf16 ring: the rounded trace
+                w32 = torch.empty(self.window[rows].shape, dtype=torch.float32, device=self.device)
+                synth.fill_query_device(w32, self.q[rows].view(torch.int16), sd, 0, self.q0,
+                                        cfg.n_q_heads)
+                self.window[rows].copy_(w32)
         self.ring_start = 0
         self.p_pred.ring_start = 0
 

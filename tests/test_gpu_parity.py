@@ -682,3 +682,26 @@ def test_predict_bf16_window():
     w8 = torch.zeros(1, 2, 8, 64, dtype=torch.bfloat16, device=DEV)
     with pytest.raises(asp.AsyncSpadeError):
         asp.predict_query(w8, flags=asp.ASSEMBLY_PER_WINDOW)
+
+
+def test_bf16_window_step_and_append():
+    """A bf16 query ring end to end: asyncspade_append rounds q_t into the
+    slot, the step predicts from it exactly as from the widened fp32 ring."""
+    cfg = configs.QWEN3_8B.with_(batch=2, seq_len=1024, top_k=128)
+    sb = DecodeStep(cfg, DEV, window_dtype=torch.bfloat16)
+    sb.fill_synthetic()
+    q_t = torch.randn(2, 32, 128, generator=torch.Generator().manual_seed(9)).to(DEV)
+    slot = sb.ring_start
+    sb.append(q_t)
+    torch.cuda.synchronize()
+    assert torch.equal(sb.window[:, :, slot], q_t.to(torch.bfloat16))
+    sf = DecodeStep(cfg, DEV)
+    sf.fill_synthetic()
+    sf.window.copy_(sb.window.float())
+    sf.q.copy_(sb.q)
+    sf.ring_start, sf.p_pred.ring_start = sb.ring_start, sb.ring_start
+    sb.run()
+    sf.run()
+    torch.cuda.synchronize()
+    assert torch.equal(sb.q_hat, sf.q_hat)
+    assert torch.equal(sb.sel_idx, sf.sel_idx) and torch.equal(sb.out, sf.out)

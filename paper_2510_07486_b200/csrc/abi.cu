@@ -8,7 +8,7 @@
 namespace {
 
 bool aligned16(const void *ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
-bool group_ok(int G) { return G == 1 || G == 2 || G == 4 || G == 8; }
+bool group_ok(int G) { return G == 1 || G == 2 || G == 4 || G == 8 || G == 16; }
 bool dim_ok(int D) { return D == 64 || D == 128; }
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -111,7 +111,8 @@ asp_status asyncspade_predict_query(const asp_predict_params *p, const float *q_
                            ASP_DOUBLE_SOFTMAX | ASP_WINDOW_BF16;
     if (mode > ASP_ASSEMBLY_PER_WINDOW || (p->flags & ~known)) return ASP_ERR_INVALID_ARGUMENT;
     if ((p->flags & ASP_WINDOW_BF16) &&
-        (p->window < 2 || p->window > 16 || mode == ASP_ASSEMBLY_PER_WINDOW))
+        (p->window < 2 || p->window > 16 || mode == ASP_ASSEMBLY_PER_WINDOW ||
+         (int64_t)p->batch * p->n_q_heads * p->window * p->head_dim >= ((int64_t)1 << 31)))
         return ASP_ERR_UNSUPPORTED;
     if ((p->flags & ASP_NORM_NONE) && mode != ASP_ASSEMBLY_SINGLE) return ASP_ERR_INVALID_ARGUMENT;
     if (!(p->eps == p->eps)) return ASP_ERR_INVALID_ARGUMENT;

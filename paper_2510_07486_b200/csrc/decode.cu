@@ -53,24 +53,26 @@ using namespace asp::tc;
 constexpr int kTile = 128;                  // tokens per tile
 constexpr int kChunk = 256;                 // entries per work item (fixed: determinism)
 constexpr int kTilesPerItem = kChunk / kTile;
-constexpr int kN = 16;                      // MMA N: G heads (MMA1) / 2G hi-lo rows (MMA2)
+constexpr int kN = 16;                      // MMA1 N: the G <= 16 query heads
 constexpr int kProducerWarps = 8;
 constexpr int kProducerThreads = kProducerWarps * 32;
 constexpr int kMmaWarp = kProducerWarps + 4;
 constexpr int kThreads = (kProducerWarps + 5) * 32;   // producers, 4 softmax/epilogue, 1 MMA warp
 constexpr float kLog2e = 1.4426950408889634f;
 
-template <int D>
+template <int D, int G>
 struct DCfg {
     static constexpr int kRegions = D / 64;
     static constexpr int kStageBytes = kRegions * kTile * 128;      // one K or V tile
     static constexpr int kStages = D == 128 ? 5 : 8;
+    static constexpr int kN2 = 2 * G <= 16 ? 16 : 32;               // MMA2 N: 2G hi/lo P rows
+    static constexpr int kGR = G <= 8 ? 8 : G;                      // reduction row stride
     static constexpr int kQSlotBytes = kRegions * kN * 128;
-    static constexpr int kPTileBytes = 2 * kN * 128;                // 128 tokens = 2 regions
+    static constexpr int kPTileBytes = 2 * kN2 * 128;               // 128 tokens = 2 regions
     static constexpr int kPSlotBytes = kTilesPerItem * kPTileBytes;
     static constexpr int kZeroBytes = D == 64 ? 16384 : 0;          // MN-block 1 of V^T for D=64
     static constexpr int kTokBytes = 2 * kChunk * 4;
-    static constexpr int kRedBytes = 2 * 2 * 4 * 8 * 4 + 2 * 8 * 4; // wmax, wsum, mrow
+    static constexpr int kRedBytes = 2 * 2 * 4 * kGR * 4 + 2 * kGR * 4; // wmax, wsum, mrow
     static constexpr int kBarBytes = 256;
     static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 2 * kQSlotBytes +
                                       2 * kPSlotBytes + kZeroBytes + kTokBytes + kRedBytes +
@@ -93,7 +95,8 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                  const asp_bf16 *__restrict__ k_cache, const asp_bf16 *__restrict__ v_cache,
                  const int32_t *__restrict__ seq_lens, const int32_t *__restrict__ sel_idx,
                  float *__restrict__ partials, int n_splits, PagedArgs pg) {
-    using C = DCfg<D>;
+    using C = DCfg<D, G>;
+    constexpr int kGR = C::kGR;
     extern __shared__ unsigned char smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -107,9 +110,9 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
     const uint32_t red0 = tok0 + C::kTokBytes;
     const uint32_t bar0 = red0 + C::kRedBytes;
     int32_t *s_tok = reinterpret_cast<int32_t *>(gb + (tok0 - base));          // [2][256]
-    float *s_wmax = reinterpret_cast<float *>(gb + (red0 - base));             // [2][4][8]
-    float *s_wsum = s_wmax + 2 * 4 * 8;                                        // [2][4][8]
-    float *s_mrow = s_wsum + 2 * 4 * 8;                                        // [2][8]
+    float *s_wmax = reinterpret_cast<float *>(gb + (red0 - base));             // [2][4][kGR]
+    float *s_wsum = s_wmax + 2 * 4 * kGR;                                      // [2][4][kGR]
+    float *s_mrow = s_wsum + 2 * 4 * kGR;                                      // [2][kGR]
     auto bar = [&](int i) { return bar0 + 8u * i; };
     // barrier indices
     const int B_FULL = 0, B_EMPTY = C::kStages;
@@ -166,7 +169,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
 #endif
     // TMEM columns: S[slot][tile] at slot*32 + tile*16, O[slot] at 64 + slot*16
     auto s_col = [](int slot, int t) { return (uint32_t)(slot * 32 + t * 16); };
-    auto o_col = [](int slot) { return (uint32_t)(64 + slot * 16); };
+    auto o_col = [](int slot) { return (uint32_t)(64 + slot * C::kN2); };
 
     if (warp < kProducerWarps) {
         // ================================================= producers (4 warps)
@@ -348,7 +351,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
         // ================================================= MMA issuer
         {                                   // whole warp; one elected lane issues
             constexpr uint32_t idesc1 = idesc_bf16_f32(kTile, kN);                 // K-major A, B
-            constexpr uint32_t idesc2 = idesc_bf16_f32(kTile, kN) | (1u << 15);    // A MN-major
+            constexpr uint32_t idesc2 = idesc_bf16_f32(kTile, C::kN2) | (1u << 15); // A MN-major
             int s = 0, qs = -1, cur_row = -1;
             uint32_t ph = 0, qph = 0;
             auto wait_stage = [&]() {
@@ -400,7 +403,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                         uint64_t ad = desc_sw128_kmajor(vb + kk * 2048);
                         ad = (ad & ~(0x3FFFull << 16)) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16);
                         const uint64_t bd = desc_sw128_kmajor(pb + t * C::kPTileBytes +
-                                                              (kk / 4) * (kN * 128) + (kk % 4) * 32);
+                                                              (kk / 4) * (C::kN2 * 128) + (kk % 4) * 32);
                         mma_bf16_warp(tmem_base + o_col(slot), ad, bd, idesc2, (t | kk) ? 1u : 0u);
                     }
                     mma_commit_warp(bar(B_EMPTY + s));
@@ -465,14 +468,14 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             }
             if (lane == 0)
 #pragma unroll
-                for (int g = 0; g < G; g++) s_wmax[(slot * 4 + quad) * 8 + g] = mx[g];
+                for (int g = 0; g < G; g++) s_wmax[(slot * 4 + quad) * kGR + g] = mx[g];
             asm volatile("bar.sync 1, 128;" ::: "memory");
             float M[G];
 #pragma unroll
             for (int g = 0; g < G; g++) {
-                float m = s_wmax[(slot * 4 + 0) * 8 + g];
+                float m = s_wmax[(slot * 4 + 0) * kGR + g];
 #pragma unroll
-                for (int w = 1; w < 4; w++) m = fmaxf(m, s_wmax[(slot * 4 + w) * 8 + g]);
+                for (int w = 1; w < 4; w++) m = fmaxf(m, s_wmax[(slot * 4 + w) * kGR + g]);
                 M[g] = m;
             }
             unsigned char *pb = gb + (pslot0 - base) + slot * C::kPSlotBytes;
@@ -483,7 +486,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             for (int g = 0; g < G; g++) sum[g] = 0.0f;
 #pragma unroll
             for (int t = 0; t < kTilesPerItem; t++) {
-                unsigned char *ptile = pb + t * C::kPTileBytes + region * (kN * 128);
+                unsigned char *ptile = pb + t * C::kPTileBytes + region * (C::kN2 * 128);
 #pragma unroll
                 for (int g = 0; g < G; g++) {
                     const float pv = (tok[t] >= 0 && M[g] != -INFINITY) ? exp2f(l[t][g] - M[g]) : 0.0f;
@@ -501,8 +504,8 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             for (int g = 0; g < G; g++) sum[g] = asp::warp_sum(sum[g]);
             if (lane == 0)
 #pragma unroll
-                for (int g = 0; g < G; g++) s_wsum[(slot * 4 + quad) * 8 + g] = sum[g];
-            if (quad == 0 && lane < G) s_mrow[slot * 8 + lane] = M[lane];
+                for (int g = 0; g < G; g++) s_wsum[(slot * 4 + quad) * kGR + g] = sum[g];
+            if (quad == 0 && lane < G) s_mrow[slot * kGR + lane] = M[lane];
             fence_proxy_async_smem();
             tc_fence_before();
             __syncwarp();
@@ -517,8 +520,11 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             const uint32_t use = (uint32_t)((i >> 1) & 1);
             DWAIT(9, mbar_wait(bar(B_OFULL + slot), use));
             tc_fence_after();
-            uint32_t r[16];
-            tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + o_col(slot), r);
+            uint32_t r[C::kN2];
+            if constexpr (C::kN2 == 32)
+                tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + o_col(slot), r);
+            else
+                tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + o_col(slot), r);
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
@@ -537,8 +543,8 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                 if (d == 0) {
                     float L = 0.0f;
 #pragma unroll
-                    for (int w = 0; w < 4; w++) L += s_wsum[(slot * 4 + w) * 8 + g];
-                    st_global_hint(dst, s_mrow[slot * 8 + g], keep);
+                    for (int w = 0; w < 4; w++) L += s_wsum[(slot * 4 + w) * kGR + g];
+                    st_global_hint(dst, s_mrow[slot * kGR + g], keep);
                     st_global_hint(dst + 1, L, keep);
                 }
             }
@@ -596,7 +602,7 @@ cudaError_t launch(const asp_decode_params &p, const asp_bf16 *q, const asp_bf16
                    const asp_bf16 *v, const int32_t *seq_lens, const int32_t *idx, float *out,
                    float *partials, cudaStream_t s, const asp_paged_kv *pk,
                    const int32_t *block_table) {
-    using C = DCfg<D>;
+    using C = DCfg<D, G>;
     const int ns = n_splits_of(p);
     const long total = (long)p.batch * p.n_kv_heads * ns;
     const int grid = (int)(total < asp_sm_count() ? total : asp_sm_count());
@@ -639,6 +645,7 @@ cudaError_t asp_launch_decode(const asp_decode_params &p, const asp_bf16 *q,
         return launch<DD, GG>(p, q, k_cache, v_cache, seq_lens, sel_idx, out, partials, s, pk, block_table);
     ASP_CASE(64, 1) ASP_CASE(64, 2) ASP_CASE(64, 4) ASP_CASE(64, 8)
     ASP_CASE(128, 1) ASP_CASE(128, 2) ASP_CASE(128, 4) ASP_CASE(128, 8)
+    ASP_CASE(64, 16) ASP_CASE(128, 16)
 #undef ASP_CASE
     return cudaErrorInvalidValue;
 }

@@ -460,7 +460,7 @@ ASP_DEV double half_softmax(double v, int l, int n) {
 // four consecutive window elements at element offset `off` (a multiple of 4)
 // as fp32: the ring is fp32, or bf16 with ASP_WINDOW_BF16 (exact widening)
 template <bool BF>
-ASP_DEV float4 ld4(const float *__restrict__ win, long off) {
+ASP_DEV float4 ld4(const float *__restrict__ win, int off) {
     if constexpr (BF) {
         const uint2 w = __ldg(reinterpret_cast<const uint2 *>(reinterpret_cast<const asp_bf16 *>(win) + off));
         return make_float4(asp::bf16lo(w.x), asp::bf16hi(w.x), asp::bf16lo(w.y), asp::bf16hi(w.y));
@@ -504,14 +504,14 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
         for (int r = 0; r < 2; r++)
 #pragma unroll
             for (int t = 0; t < T; t++) acc[r][t][0] = acc[r][t][1] = acc2[r][t][0] = acc2[r][t][1] = 0.0;
-        long rp[2][NB];                                 // element offsets (-1: padding)
-#pragma unroll
+        int rp[2][NB];                                  // element offsets (-1: padding;
+#pragma unroll                                          //  the window is < 2^31 elements)
         for (int r = 0; r < 2; r++)
 #pragma unroll
             for (int b = 0; b < NB; b++) {
                 const int i = 8 * b + fr;
                 const bool live = i < W && (r == 0 || has1);
-                rp[r][b] = live ? (long)(row0 + r) * W * D + (long)phys_of(i) * D + 4 * fc : -1;
+                rp[r][b] = live ? ((int)row0 + r) * W * D + phys_of(i) * D + 4 * fc : -1;
             }
         // software-pipelined: the next two groups' fragments are in flight while
         // this pair's MMAs run (the loads, not the MMAs, set the latency).  The
@@ -703,7 +703,7 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
     // ---- q_hat = (1/m) sum_p c_p Q[p] (one pass over the cache-hot window), or
     // the passthrough Q_t.
     const bool live = h == 0 || has1;
-    const long src = (long)(row0 + h) * W * D;                         // element offset
+    const int src = ((int)row0 + h) * W * D;                           // element offset
     float *out = q_hat + (size_t)(row0 + h) * D;
     constexpr int kV = D / 64;                                          // float4 per lane
     // (all lanes run the loop -- its shuffles span both halves -- even when a
@@ -715,7 +715,7 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
         for (int z = 0; z < 4; z++) acc[u][z] = acc2[u][z] = 0.0;
     auto axpy = [&](double (&a)[kV][4], int q) {
         const double cq = shfl16(c, q - 1);
-        const long rq = src + (long)phys_of(q) * D + 4 * l;
+        const int rq = src + phys_of(q) * D + 4 * l;
 #pragma unroll
         for (int u = 0; u < kV; u++) {
             const float4 v4 = live ? ld4<BF>(q_window, rq + 64 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -743,7 +743,7 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
                 make_float4((float)(acc[u][0] * inv_m), (float)(acc[u][1] * inv_m),
                             (float)(acc[u][2] * inv_m), (float)(acc[u][3] * inv_m));
     } else if (live) {
-        const long rq = src + (long)phys_of(W - 1) * D + 4 * l;
+        const int rq = src + phys_of(W - 1) * D + 4 * l;
 #pragma unroll
         for (int u = 0; u < kV; u++) reinterpret_cast<float4 *>(out)[l + 16 * u] = ld4<BF>(q_window, rq + 64 * u);
         if (l == 0) asp::flag_or(dev_flags, finite ? ASP_FLAG_NOT_PD : ASP_FLAG_NONFINITE);
@@ -789,7 +789,8 @@ cudaError_t asp_launch_predict(const asp_predict_params &p, const float *q_windo
                                uint32_t *dev_flags, cudaStream_t s) {
     const int nb = (p.window + 7) / 8;
     const uint32_t mode = p.flags & 0xFu;
-    if (p.window >= 2 && p.window <= 16 &&
+    const bool small = (long)p.batch * p.n_q_heads * p.window * p.head_dim < (1L << 31);
+    if (p.window >= 2 && p.window <= 16 && small &&
         (mode == ASP_ASSEMBLY_MASKED_SHARED || mode == ASP_ASSEMBLY_SINGLE)) {
         if (p.head_dim == 64) return nb == 1 ? launch_pair<64, 1>(p, q_window, q_hat, dev_flags, s)
                                              : launch_pair<64, 2>(p, q_window, q_hat, dev_flags, s);

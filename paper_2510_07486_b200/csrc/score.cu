@@ -71,6 +71,8 @@ struct Cfg {
     static constexpr int kStageBytes = kTileM * D * 2;
     static constexpr int kBRegionBytes = N * 128;
     static constexpr int kBSlotBytes = kRegions * kBRegionBytes;
+    // accumulator stages: 6, or 5 when 6 would not fit the 512 TMEM columns (G = 16)
+    static constexpr int kAcc = (2 * ::kAcc * N) <= 512 ? ::kAcc : 512 / (2 * N);
     static constexpr uint32_t kTmemCols = (2 * kAcc * N) <= 64 ? 64 : (2 * kAcc * N) <= 128 ? 128
                                           : (2 * kAcc * N) <= 256 ? 256 : 512;
     static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes +
@@ -239,10 +241,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
     auto empty_bar = [&](int s) { return bar0 + 8u * (kStages + s); };
     auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * kStages + a); };
-    auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * kStages + kAcc + a); };
-    auto bfull_bar = [&](int s) { return bar0 + 8u * (2 * kStages + 2 * kAcc + s); };
-    auto bempty_bar = [&](int s) { return bar0 + 8u * (2 * kStages + 2 * kAcc + kBSlots + s); };
-    const uint32_t tmem_holder = bar0 + 8u * (2 * kStages + 2 * kAcc + 2 * kBSlots);
+    auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * kStages + C::kAcc + a); };
+    auto bfull_bar = [&](int s) { return bar0 + 8u * (2 * kStages + 2 * C::kAcc + s); };
+    auto bempty_bar = [&](int s) { return bar0 + 8u * (2 * kStages + 2 * C::kAcc + kBSlots + s); };
+    const uint32_t tmem_holder = bar0 + 8u * (2 * kStages + 2 * C::kAcc + 2 * kBSlots);
     unsigned char *gbslot0 = gbase + (bslot0 - base);
     volatile uint32_t *tmem_holder_g =
         reinterpret_cast<volatile uint32_t *>(gbase + (tmem_holder - base));
@@ -306,7 +308,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; s++) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
-        for (int a = 0; a < kAcc; a++) { mbar_init(tfull_bar(a), 1); mbar_init(tempty_bar(a), 4); }
+        for (int a = 0; a < C::kAcc; a++) { mbar_init(tfull_bar(a), 1); mbar_init(tempty_bar(a), 4); }
         for (int s = 0; s < kBSlots; s++) { mbar_init(bfull_bar(s), 1); mbar_init(bempty_bar(s), 1); }
         fence_mbar_init();
         prefetch_tmap(&kmap);
@@ -429,7 +431,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
                     ga[ng] = a;
                     ng++;
                     if (++s == kStages) { s = 0; ph ^= 1; }
-                    if (++a == kAcc) { a = 0; aph ^= 1; }
+                    if (++a == C::kAcc) { a = 0; aph ^= 1; }
                     i = it.next(i + 1);
                 }
 #ifdef ASP_PROFILE_SCORE
@@ -538,8 +540,8 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
         const uint64_t keep = l2_policy_evict_last();
         for (long i = it.next(it.start); i < it.end; i = it.next(i + 1), k++) {
             if ((k & 1) != group) continue;
-            const int a = (int)(k % kAcc);
-            const uint32_t aph = (uint32_t)((k / kAcc) & 1);
+            const int a = (int)(k % C::kAcc);
+            const uint32_t aph = (uint32_t)((k / C::kAcc) & 1);
             const int row = it.row, j = it.j;
             PWAIT(pe_full, mbar_wait(tfull_bar(a), aph));
             tc_fence_after();
@@ -552,6 +554,17 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
                 tmem_wait_ld();
 #pragma unroll
                 for (int c = 0; c < 32; c++) v[c] = __fadd_rn(__uint_as_float(r0[c]), __uint_as_float(r1[c]));
+            } else if constexpr (N == 48) {
+                uint32_t r0[32], r1[32], r2[16], r3[16];
+                tmem_ld32(taddr, r0);
+                tmem_ld16(taddr + 32, r2);
+                tmem_ld32(taddr + N, r1);
+                tmem_ld16(taddr + N + 32, r3);
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 32; c++) v[c] = __fadd_rn(__uint_as_float(r0[c]), __uint_as_float(r1[c]));
+#pragma unroll
+                for (int c = 0; c < 16; c++) v[32 + c] = __fadd_rn(__uint_as_float(r2[c]), __uint_as_float(r3[c]));
             } else {
                 uint32_t r0[16], r1[16];
                 tmem_ld16(taddr, r0);
@@ -661,6 +674,7 @@ cudaError_t asp_launch_score(const asp_select_params &p, const float *q_hat,
         return launch<DD, GG>(p, q_hat, k_cache, seq_lens, scores, dev_flags, s, pk, block_table);
     ASP_CASE(64, 1) ASP_CASE(64, 2) ASP_CASE(64, 4) ASP_CASE(64, 8)
     ASP_CASE(128, 1) ASP_CASE(128, 2) ASP_CASE(128, 4) ASP_CASE(128, 8)
+    ASP_CASE(64, 16) ASP_CASE(128, 16)
 #undef ASP_CASE
     return cudaErrorInvalidValue;
 }

@@ -114,7 +114,7 @@ def _score_select_case(B, Hq, Hkv, D, L, k, seq_lens, seed, kv=None, agg=asp.AGG
     return idx.cpu().numpy(), scores.cpu().numpy(), s_or, int(flags.item())
 
 
-@pytest.mark.parametrize("G", [1, 2, 4, 8])
+@pytest.mark.parametrize("G", [1, 2, 4, 8, 16])
 @pytest.mark.parametrize("D", [64, 128])
 def test_score_select_parity_small(G, D):
     B, Hkv, L, k = 3, 2, 1000, 37
@@ -215,7 +215,7 @@ def _decode_case(B, Hq, Hkv, D, L, idx, seq_lens, n_fresh, seed):
     return out.cpu().numpy(), ref, (q, K, V)
 
 
-@pytest.mark.parametrize("G", [1, 2, 4, 8])
+@pytest.mark.parametrize("G", [1, 2, 4, 8, 16])
 @pytest.mark.parametrize("D", [64, 128])
 @pytest.mark.parametrize("n_fresh", [0, 1, 3])
 def test_decode_parity(G, D, n_fresh):
@@ -705,3 +705,16 @@ def test_bf16_window_step_and_append():
     torch.cuda.synchronize()
     assert torch.equal(sb.q_hat, sf.q_hat)
     assert torch.equal(sb.sel_idx, sf.sel_idx) and torch.equal(sb.out, sf.out)
+
+
+def test_step_group16_sampled_rows():
+    """NEXT-3: GQA group of 16 (e.g. 128 query / 8 KV heads) through the whole
+    step -- score (5 TMEM accumulator stages), select, decode (32-row P
+    operand) -- against the oracle on sampled rows."""
+    cfg = configs.Config("g16", 0, 2, 32, 2, 128, 4096, 256, 16)
+    step = DecodeStep(cfg, DEV)
+    step.fill_synthetic()
+    step.run()
+    torch.cuda.synchronize()
+    assert int(step.dev_flags.item()) == 0
+    _oracle_row_checks(step, range(cfg.batch * cfg.n_kv_heads))

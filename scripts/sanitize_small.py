@@ -1,0 +1,27 @@
+"""A small composed step of every entry point, for compute-sanitizer runs:
+append -> predict -> score_select (dense and paged) -> decode -> gather ->
+quest, on a ragged two-sequence batch."""
+import os, sys, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2510_07486_b200 as asp
+from paper_2510_07486_b200 import configs
+from paper_2510_07486_b200.step import DecodeStep
+cfg = configs.QWEN3_8B.with_(batch=2, seq_len=1024, top_k=128)
+st = DecodeStep(cfg, "cuda", n_fresh=1)
+st.fill_synthetic()
+st.seq_lens.copy_(torch.tensor([1024, 700], dtype=torch.int32))
+g = torch.Generator().manual_seed(1)
+st.append(torch.randn(2, 32, 128, generator=g).cuda(),
+          torch.randn(2, 8, 128, generator=g).to(torch.bfloat16).cuda(),
+          torch.randn(2, 8, 128, generator=g).to(torch.bfloat16).cuda(),
+          torch.tensor([1023, 699], dtype=torch.int32, device="cuda"))
+st.run()
+pool, bt = asp.page_pool(st.k_cache, 16, torch.Generator().manual_seed(2))
+vpool, _ = asp.page_pool(st.v_cache, 16, torch.Generator().manual_seed(2))
+idx = asp.score_select_paged(st.q_hat, pool, bt, st.seq_lens, cfg.top_k, cfg.seq_len)
+asp.sparse_decode_paged(st.q, pool, vpool, bt, st.seq_lens, idx, cfg.seq_len, n_fresh=1)
+asp.gather_filtered(st.k_cache, st.v_cache, st.seq_lens, st.sel_idx, n_fresh=1)
+meta = asp.quest_summarize(st.k_cache, st.seq_lens, 16, cfg.top_k, 32)
+asp.quest_select(st.q_hat, meta, st.k_cache, st.seq_lens, cfg.top_k, 16)
+torch.cuda.synchronize()
+print("sanitize-small ok, flags", int(st.dev_flags.item()))

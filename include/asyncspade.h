@@ -31,7 +31,7 @@
  *   asp_status BEFORE enqueuing anything if they are invalid: null
  *   pointers, non-positive sizes, n_q_heads % n_kv_heads != 0, unsupported
  *   head_dim (64 or 128) / group size G = n_q_heads / n_kv_heads (1, 2, 4,
- *   8, 16) / window (1..32), misaligned pointers (16 B), strides not multiples
+ *   8, 16, 32) / window (1..32), misaligned pointers (16 B), strides not multiples
  *   of 8 elements, too-small workspace.  Launch failures return
  *   ASP_ERR_CUDA.  Numeric conditions never fail a call: they OR a bit into
  *   the optional device word `dev_flags` and produce the defined fallback

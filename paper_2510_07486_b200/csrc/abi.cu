@@ -8,7 +8,7 @@
 namespace {
 
 bool aligned16(const void *ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
-bool group_ok(int G) { return G == 1 || G == 2 || G == 4 || G == 8 || G == 16; }
+bool group_ok(int G) { return G == 1 || G == 2 || G == 4 || G == 8 || G == 16 || G == 32; }
 bool dim_ok(int D) { return D == 64 || D == 128; }
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 

@@ -53,7 +53,7 @@ using namespace asp::tc;
 constexpr int kTile = 128;                  // tokens per tile
 constexpr int kChunk = 256;                 // entries per work item (fixed: determinism)
 constexpr int kTilesPerItem = kChunk / kTile;
-constexpr int kN = 16;                      // MMA1 N: the G <= 16 query heads
+
 constexpr int kProducerWarps = 8;
 constexpr int kProducerThreads = kProducerWarps * 32;
 constexpr int kMmaWarp = kProducerWarps + 4;
@@ -64,8 +64,11 @@ template <int D, int G>
 struct DCfg {
     static constexpr int kRegions = D / 64;
     static constexpr int kStageBytes = kRegions * kTile * 128;      // one K or V tile
-    static constexpr int kStages = D == 128 ? 5 : 8;
-    static constexpr int kN2 = 2 * G <= 16 ? 16 : 32;               // MMA2 N: 2G hi/lo P rows
+    static constexpr int kN = G <= 16 ? 16 : 32;                    // MMA1 N: the G query heads
+    static constexpr int kN2 = 2 * G <= 16 ? 16 : 2 * G;            // MMA2 N: 2G hi/lo P rows
+    // K/V ring: 5 (D = 128) / 8 (D = 64) stages, 4 when G = 32's P and Q slots need the room
+    static constexpr int kStages = G > 16 ? (D == 128 ? 4 : 6) : (D == 128 ? 5 : 8);
+    static constexpr uint32_t kTmemCols = 4 * kN + 2 * kN2 <= 128 ? 128 : 256;
     static constexpr int kGR = G <= 8 ? 8 : G;                      // reduction row stride
     static constexpr int kQSlotBytes = kRegions * kN * 128;
     static constexpr int kPTileBytes = 2 * kN2 * 128;               // 128 tokens = 2 regions
@@ -157,7 +160,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
     for (uint32_t o = threadIdx.x * 16; o < 2u * C::kPSlotBytes + C::kZeroBytes; o += kThreads * 16)
         *reinterpret_cast<uint4 *>(gb + (pslot0 - base) + o) = make_uint4(0, 0, 0, 0);
     fence_proxy_async_smem();
-    if (warp == kMmaWarp) tmem_alloc<128>(tmem_holder);
+    if (warp == kMmaWarp) tmem_alloc<C::kTmemCols>(tmem_holder);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -168,8 +171,8 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
     const long long t_k0 = clock64();
 #endif
     // TMEM columns: S[slot][tile] at slot*32 + tile*16, O[slot] at 64 + slot*16
-    auto s_col = [](int slot, int t) { return (uint32_t)(slot * 32 + t * 16); };
-    auto o_col = [](int slot) { return (uint32_t)(64 + slot * C::kN2); };
+    auto s_col = [](int slot, int t) { return (uint32_t)(slot * 2 * C::kN + t * C::kN); };
+    auto o_col = [](int slot) { return (uint32_t)(4 * C::kN + slot * C::kN2); };
 
     if (warp < kProducerWarps) {
         // ================================================= producers (4 warps)
@@ -256,12 +259,12 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                 DWAIT(0, mbar_wait(bar(B_QEMPTY + qs), qph ^ 1));
                 const asp_bf16 *qsrc = q + ((size_t)b * Hq + (size_t)h * G) * D;
                 unsigned char *qslot = gb + (qslot0 - base) + qs * C::kQSlotBytes;
-                for (int c = pt; c < kN * D / 8; c += kProducerThreads) {
+                for (int c = pt; c < C::kN * D / 8; c += kProducerThreads) {
                     const int n = c / (D / 8), d0 = (c % (D / 8)) * 8;
                     uint4 v = make_uint4(0, 0, 0, 0);
                     if (n < G) v = *reinterpret_cast<const uint4 *>(qsrc + n * D + d0);
                     const int region = d0 / 64, chunk = (d0 % 64) / 8;
-                    *reinterpret_cast<uint4 *>(qslot + region * (kN * 128) + n * 128 +
+                    *reinterpret_cast<uint4 *>(qslot + region * (C::kN * 128) + n * 128 +
                                                ((chunk ^ (n & 7)) * 16)) = v;
                 }
                 fence_proxy_async_smem();
@@ -350,7 +353,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
     } else if (warp == kMmaWarp) {
         // ================================================= MMA issuer
         {                                   // whole warp; one elected lane issues
-            constexpr uint32_t idesc1 = idesc_bf16_f32(kTile, kN);                 // K-major A, B
+            constexpr uint32_t idesc1 = idesc_bf16_f32(kTile, C::kN);                 // K-major A, B
             constexpr uint32_t idesc2 = idesc_bf16_f32(kTile, C::kN2) | (1u << 15); // A MN-major
             int s = 0, qs = -1, cur_row = -1;
             uint32_t ph = 0, qph = 0;
@@ -378,7 +381,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                         const int r = kk / 4, ko = (kk % 4) * 32;
                         mma_bf16_warp(tmem_base + s_col(slot, t),
                                  desc_sw128_kmajor(ab + r * (kTile * 128) + ko),
-                                 desc_sw128_kmajor(qb + r * (kN * 128) + ko), idesc1, kk > 0 ? 1u : 0u);
+                                 desc_sw128_kmajor(qb + r * (C::kN * 128) + ko), idesc1, kk > 0 ? 1u : 0u);
                     }
                     mma_commit_warp(bar(B_EMPTY + s));
                     if (++s == C::kStages) { s = 0; ph ^= 1; }
@@ -432,8 +435,11 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             int tok[kTilesPerItem];
 #pragma unroll
             for (int t = 0; t < kTilesPerItem; t++) {
-                uint32_t r[16];
-                tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + s_col(slot, t), r);
+                uint32_t r[C::kN];
+                if constexpr (C::kN == 32)
+                    tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + s_col(slot, t), r);
+                else
+                    tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + s_col(slot, t), r);
                 tmem_wait_ld();
                 tok[t] = s_tok[slot * kChunk + t * kTile + quad * 32 + lane];
 #pragma unroll
@@ -521,10 +527,18 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             DWAIT(9, mbar_wait(bar(B_OFULL + slot), use));
             tc_fence_after();
             uint32_t r[C::kN2];
-            if constexpr (C::kN2 == 32)
-                tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + o_col(slot), r);
-            else
-                tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + o_col(slot), r);
+            if constexpr (C::kN2 == 64) {
+                uint32_t (&ra)[32] = *reinterpret_cast<uint32_t (*)[32]>(&r[0]);
+                uint32_t (&rb)[32] = *reinterpret_cast<uint32_t (*)[32]>(&r[32]);
+                tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + o_col(slot), ra);
+                tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + o_col(slot) + 32, rb);
+            } else if constexpr (C::kN2 == 32) {
+                tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + o_col(slot),
+                          *reinterpret_cast<uint32_t (*)[32]>(&r[0]));
+            } else {
+                tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + o_col(slot),
+                          *reinterpret_cast<uint32_t (*)[16]>(&r[0]));
+            }
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
@@ -557,7 +571,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == kMmaWarp) tmem_dealloc<128>(tmem_base);
+    if (warp == kMmaWarp) tmem_dealloc<C::kTmemCols>(tmem_base);
 #ifdef ASP_PROFILE_DECODE
     if (threadIdx.x == 0) atomicAdd(&g_dec_prof[10], (unsigned long long)(clock64() - t_k0));
 #endif
@@ -645,7 +659,7 @@ cudaError_t asp_launch_decode(const asp_decode_params &p, const asp_bf16 *q,
         return launch<DD, GG>(p, q, k_cache, v_cache, seq_lens, sel_idx, out, partials, s, pk, block_table);
     ASP_CASE(64, 1) ASP_CASE(64, 2) ASP_CASE(64, 4) ASP_CASE(64, 8)
     ASP_CASE(128, 1) ASP_CASE(128, 2) ASP_CASE(128, 4) ASP_CASE(128, 8)
-    ASP_CASE(64, 16) ASP_CASE(128, 16)
+    ASP_CASE(64, 16) ASP_CASE(128, 16) ASP_CASE(64, 32) ASP_CASE(128, 32)
 #undef ASP_CASE
     return cudaErrorInvalidValue;
 }

@@ -71,11 +71,16 @@ struct Cfg {
     static constexpr int kStageBytes = kTileM * D * 2;
     static constexpr int kBRegionBytes = N * 128;
     static constexpr int kBSlotBytes = kRegions * kBRegionBytes;
-    // accumulator stages: 6, or 5 when 6 would not fit the 512 TMEM columns (G = 16)
+    // accumulator stages: 6, or as many as fit the 512 TMEM columns (G = 16: 5, G = 32: 2)
     static constexpr int kAcc = (2 * ::kAcc * N) <= 512 ? ::kAcc : 512 / (2 * N);
+    // K ring: 6 stages, fewer when the B-operand ring needs the room (G = 32: 5)
+    static constexpr int kStages =
+        (1024 + ::kStages * kTileM * D * 2 + kBSlots * (D / 64) * N * 128 + 256) <= 227 * 1024
+            ? ::kStages
+            : (227 * 1024 - 1024 - kBSlots * (D / 64) * N * 128 - 256) / (kTileM * D * 2);
     static constexpr uint32_t kTmemCols = (2 * kAcc * N) <= 64 ? 64 : (2 * kAcc * N) <= 128 ? 128
                                           : (2 * kAcc * N) <= 256 ? 256 : 512;
-    static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes +
+    static constexpr int kSmemBytes = 1024 /*align slack*/ + Cfg::kStages * kStageBytes +
                                       kBSlots * kBSlotBytes + 256 /*barriers*/;
 };
 
@@ -236,15 +241,15 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
     const uint32_t base = (raw + 1023u) & ~1023u;
     unsigned char *gbase = smem_raw + (base - raw);
     const uint32_t stage0 = base;
-    const uint32_t bslot0 = stage0 + kStages * C::kStageBytes;
+    const uint32_t bslot0 = stage0 + C::kStages * C::kStageBytes;
     const uint32_t bar0 = bslot0 + kBSlots * C::kBSlotBytes;
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
-    auto empty_bar = [&](int s) { return bar0 + 8u * (kStages + s); };
-    auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * kStages + a); };
-    auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * kStages + C::kAcc + a); };
-    auto bfull_bar = [&](int s) { return bar0 + 8u * (2 * kStages + 2 * C::kAcc + s); };
-    auto bempty_bar = [&](int s) { return bar0 + 8u * (2 * kStages + 2 * C::kAcc + kBSlots + s); };
-    const uint32_t tmem_holder = bar0 + 8u * (2 * kStages + 2 * C::kAcc + 2 * kBSlots);
+    auto empty_bar = [&](int s) { return bar0 + 8u * (C::kStages + s); };
+    auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * C::kStages + a); };
+    auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * C::kStages + C::kAcc + a); };
+    auto bfull_bar = [&](int s) { return bar0 + 8u * (2 * C::kStages + 2 * C::kAcc + s); };
+    auto bempty_bar = [&](int s) { return bar0 + 8u * (2 * C::kStages + 2 * C::kAcc + kBSlots + s); };
+    const uint32_t tmem_holder = bar0 + 8u * (2 * C::kStages + 2 * C::kAcc + 2 * kBSlots);
     unsigned char *gbslot0 = gbase + (bslot0 - base);
     volatile uint32_t *tmem_holder_g =
         reinterpret_cast<volatile uint32_t *>(gbase + (tmem_holder - base));
@@ -307,7 +312,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
     it.max_len = p.max_seq_len;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; s++) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
+        for (int s = 0; s < C::kStages; s++) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
         for (int a = 0; a < C::kAcc; a++) { mbar_init(tfull_bar(a), 1); mbar_init(tempty_bar(a), 4); }
         for (int s = 0; s < kBSlots; s++) { mbar_init(bfull_bar(s), 1); mbar_init(bempty_bar(s), 1); }
         fence_mbar_init();
@@ -344,7 +349,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
                 for (int r = 0; r < C::kRegions; r++)
                     tma_load_2d(dst + r * (kTileM * 128), &kmap, full_bar(s), r * 64, grow,
                                 kEvictFirst);
-                if (++s == kStages) { s = 0; ph ^= 1; }
+                if (++s == C::kStages) { s = 0; ph ^= 1; }
             }
             PFLUSH(0, pw_empty);
         }
@@ -396,7 +401,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
                     tma_load_2d(dst + r * (kTileM * 128) + lane * P * 128, &kmap, full_bar(s),
                                 r * 64, (cur * p.n_kv_heads + h) * P, kEvictFirst);
             }
-            if (++s == kStages) { s = 0; ph ^= 1; }
+            if (++s == C::kStages) { s = 0; ph ^= 1; }
         }
         __syncwarp();
     } else if (warp == 1) {
@@ -430,7 +435,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
                     gs[ng] = s;
                     ga[ng] = a;
                     ng++;
-                    if (++s == kStages) { s = 0; ph ^= 1; }
+                    if (++s == C::kStages) { s = 0; ph ^= 1; }
                     if (++a == C::kAcc) { a = 0; aph ^= 1; }
                     i = it.next(i + 1);
                 }
@@ -554,6 +559,24 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
                 tmem_wait_ld();
 #pragma unroll
                 for (int c = 0; c < 32; c++) v[c] = __fadd_rn(__uint_as_float(r0[c]), __uint_as_float(r1[c]));
+            } else if constexpr (N == 96) {
+                // G = 32: the three 32-column chunks are the hi / mid / lo terms;
+                // s_g = (hi_g + mid_g) + lo_g accumulated chunk by chunk
+                uint32_t r0[32], r1[32];
+                float acc32[32];
+#pragma unroll
+                for (int c = 0; c < 3; c++) {
+                    tmem_ld32(taddr + 32 * c, r0);
+                    tmem_ld32(taddr + N + 32 * c, r1);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int g = 0; g < 32; g++) {
+                        const float x = __fadd_rn(__uint_as_float(r0[g]), __uint_as_float(r1[g]));
+                        acc32[g] = c == 0 ? x : __fadd_rn(acc32[g], x);
+                    }
+                }
+#pragma unroll
+                for (int g = 0; g < 32; g++) v[g] = acc32[g];
             } else if constexpr (N == 48) {
                 uint32_t r0[32], r1[32], r2[16], r3[16];
                 tmem_ld32(taddr, r0);
@@ -579,7 +602,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
             float s = 0.0f;
 #pragma unroll
             for (int g = 0; g < G; g++) {
-                const float sg = __fadd_rn(__fadd_rn(v[g], v[G + g]), v[2 * G + g]);
+                const float sg = N == 96 ? v[g] : __fadd_rn(__fadd_rn(v[g], v[G + g]), v[2 * G + g]);
                 s = g == 0 ? sg : (p.aggregation == ASP_AGG_SUM ? __fadd_rn(s, sg) : fmaxf(s, sg));
             }
             const int tok = j * kTileM + quad * 32 + lane;
@@ -674,7 +697,7 @@ cudaError_t asp_launch_score(const asp_select_params &p, const float *q_hat,
         return launch<DD, GG>(p, q_hat, k_cache, seq_lens, scores, dev_flags, s, pk, block_table);
     ASP_CASE(64, 1) ASP_CASE(64, 2) ASP_CASE(64, 4) ASP_CASE(64, 8)
     ASP_CASE(128, 1) ASP_CASE(128, 2) ASP_CASE(128, 4) ASP_CASE(128, 8)
-    ASP_CASE(64, 16) ASP_CASE(128, 16)
+    ASP_CASE(64, 16) ASP_CASE(128, 16) ASP_CASE(64, 32) ASP_CASE(128, 32)
 #undef ASP_CASE
     return cudaErrorInvalidValue;
 }

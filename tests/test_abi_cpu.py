@@ -89,7 +89,7 @@ def test_score_select_validation_and_workspace(L):
     assert call(p, ws=FAKE + 16) == 4                          # workspace must be 256-B aligned
     assert call(_sel(n_q_heads=30)) == 2
     assert call(_sel(top_k=0)) == 2
-    assert call(_sel(n_q_heads=256)) == 3                      # G = 32 (not built)
+    assert call(_sel(n_q_heads=512)) == 3                      # G = 64 (not built)
     assert call(_sel(head_dim=256, k_stride_t=256)) == 3
     assert call(_sel(aggregation=2)) == 1
     assert call(_sel(k_stride_t=100)) == 2                     # shorter than a row

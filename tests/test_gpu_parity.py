@@ -114,7 +114,7 @@ def _score_select_case(B, Hq, Hkv, D, L, k, seq_lens, seed, kv=None, agg=asp.AGG
     return idx.cpu().numpy(), scores.cpu().numpy(), s_or, int(flags.item())
 
 
-@pytest.mark.parametrize("G", [1, 2, 4, 8, 16])
+@pytest.mark.parametrize("G", [1, 2, 4, 8, 16, 32])
 @pytest.mark.parametrize("D", [64, 128])
 def test_score_select_parity_small(G, D):
     B, Hkv, L, k = 3, 2, 1000, 37
@@ -215,7 +215,7 @@ def _decode_case(B, Hq, Hkv, D, L, idx, seq_lens, n_fresh, seed):
     return out.cpu().numpy(), ref, (q, K, V)
 
 
-@pytest.mark.parametrize("G", [1, 2, 4, 8, 16])
+@pytest.mark.parametrize("G", [1, 2, 4, 8, 16, 32])
 @pytest.mark.parametrize("D", [64, 128])
 @pytest.mark.parametrize("n_fresh", [0, 1, 3])
 def test_decode_parity(G, D, n_fresh):
@@ -718,3 +718,16 @@ def test_step_group16_sampled_rows():
     torch.cuda.synchronize()
     assert int(step.dev_flags.item()) == 0
     _oracle_row_checks(step, range(cfg.batch * cfg.n_kv_heads))
+
+
+def test_step_mqa_group32_sampled_rows():
+    """NEXT-3: multi-query attention -- 32 query heads on ONE KV head (G = 32:
+    score N = 96 with 2 TMEM accumulator stages and a 5-stage K ring, decode
+    with a 64-row P operand and 256 TMEM columns) -- against the oracle."""
+    cfg = configs.Config("mqa32", 0, 3, 32, 1, 128, 4096, 256, 16)
+    step = DecodeStep(cfg, DEV, n_fresh=1)
+    step.fill_synthetic()
+    step.run()
+    torch.cuda.synchronize()
+    assert int(step.dev_flags.item()) == 0
+    _oracle_row_checks(step, range(cfg.batch * cfg.n_kv_heads), n_fresh=1)

@@ -1,6 +1,6 @@
 """A small composed step of every entry point, for compute-sanitizer runs:
 append -> predict -> score_select (dense and paged) -> decode -> gather ->
-quest, on a ragged two-sequence batch."""
+quest, on a ragged two-sequence batch; then full steps at G = 16 and G = 32."""
 import os, sys, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2510_07486_b200 as asp
@@ -23,5 +23,13 @@ asp.sparse_decode_paged(st.q, pool, vpool, bt, st.seq_lens, idx, cfg.seq_len, n_
 asp.gather_filtered(st.k_cache, st.v_cache, st.seq_lens, st.sel_idx, n_fresh=1)
 meta = asp.quest_summarize(st.k_cache, st.seq_lens, 16, cfg.top_k, 32)
 asp.quest_select(st.q_hat, meta, st.k_cache, st.seq_lens, cfg.top_k, 16)
+# GQA group 16 and 32-head MQA (the largest P / Q operands and TMEM layouts)
+for G, hkv in ((16, 2), (32, 1)):
+    c2 = configs.Config(f"g{G}", 0, 2, G * hkv, hkv, 128, 2048, 256, 16)
+    s2 = DecodeStep(c2, "cuda", n_fresh=1)
+    s2.fill_synthetic()
+    s2.run()
+    flags = int(s2.dev_flags.item())
+    assert flags == 0, flags
 torch.cuda.synchronize()
 print("sanitize-small ok, flags", int(st.dev_flags.item()))

@@ -429,7 +429,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
                 }
                 // collect a group of consecutive valid tiles of this row
                 int gs[kGroup], ga[kGroup], ng = 0;
-                while (ng < kGroup && i < it.end && it.row == row) {
+                // (a group never needs more accumulator stages than exist: every
+                // tile of it waits for its stage before any of them is issued)
+                constexpr int kGroupMax = C::kAcc < kGroup ? C::kAcc : kGroup;
+                while (ng < kGroupMax && i < it.end && it.row == row) {
                     PWAIT(pm_full, mbar_wait(full_bar(s), ph));
                     PWAIT(pm_tempty, mbar_wait(tempty_bar(a), aph ^ 1));
                     gs[ng] = s;

@@ -161,7 +161,7 @@ def quest_point(cfg, args, P=16):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("sweep", choices=["long-cot", "high-concurrency", "layer-packed", "quest",
-                                      "gather"])
+                                      "gather", "groups"])
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--out", default=None)
@@ -181,6 +181,14 @@ def main():
         # token top-k of the current query.
         for cfg in (configs.QWEN3_8B, configs.QWEN3_32B):
             lines.append(quest_point(cfg, args))
+            print(json.dumps(lines[-1]), flush=True)
+    elif args.sweep == "groups":
+        # GQA group size 1..32 at a fixed KV cache (B = 16, 8 KV heads, 32k, k = 2048): the
+        # score stream stays HBM-bound as G (the contraction's intensity) grows
+        for G in (1, 2, 4, 8, 16, 32):
+            cfg = configs.Config(f"groups_g{G}_b16_ctx32k", 2, 16, 8 * G, 8, 128, 32768, 2048, 16)
+            lines.append(point(cfg, args))
+            lines[-1]["group"] = G
             print(json.dumps(lines[-1]), flush=True)
     elif args.sweep == "gather":
         # NEXT-1: the Cache Rank's payload (asyncspade_gather_filtered) per layer

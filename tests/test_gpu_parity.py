@@ -731,3 +731,15 @@ def test_step_mqa_group32_sampled_rows():
     torch.cuda.synchronize()
     assert int(step.dev_flags.item()) == 0
     _oracle_row_checks(step, range(cfg.batch * cfg.n_kv_heads), n_fresh=1)
+
+
+@pytest.mark.parametrize("G", [16, 32])
+def test_score_select_large_groups_multi_tile_ranges(G):
+    """G = 16 / 32 with several 128-token tiles per persistent CTA (the MMA
+    issuer groups tiles; G = 32 has only 2 TMEM accumulator stages): band-rule
+    parity on every row against the oracle."""
+    B, Hkv, D, L, k = 2, 1, 128, 32768, 2048
+    lens = [L, 20000]
+    idx, _, s_or, flags = _score_select_case(B, Hkv * G, Hkv, D, L, k, lens, seed=400 + G)
+    for b in range(B):
+        check_selection(idx[b, 0], s_or[b, 0], lens[b], k)

@@ -743,3 +743,19 @@ def test_score_select_large_groups_multi_tile_ranges(G):
     idx, _, s_or, flags = _score_select_case(B, Hkv * G, Hkv, D, L, k, lens, seed=400 + G)
     for b in range(B):
         check_selection(idx[b, 0], s_or[b, 0], lens[b], k)
+
+
+@pytest.mark.parametrize("G", [16, 32])
+def test_step_large_groups_multi_item(G):
+    """G = 16 / 32 through the whole step with several decode work items and
+    score tiles per persistent CTA (the pipelined slot / phase paths), sampled
+    rows against the oracle."""
+    cfg = configs.Config(f"g{G}_multi", 0, 4, 8 * G, 8, 128, 8192, 2048, 16)
+    step = DecodeStep(cfg, DEV)
+    step.fill_synthetic()
+    step.run()
+    torch.cuda.synchronize()
+    assert int(step.dev_flags.item()) == 0
+    _oracle_row_checks(step, rows_sample(cfg.batch * cfg.n_kv_heads, 4, seed=G))
+    del step
+    torch.cuda.empty_cache()

@@ -184,7 +184,16 @@ ASP_API asp_status asyncspade_predict_query(const asp_predict_params *p, const f
  *           k_stride_b and k_stride_h must be multiples of k_stride_t (the
  *           kernel streams the cache as TMA tiles of a [rows][head_dim]
  *           view), else ASP_ERR_UNSUPPORTED.
- * seq_lens  device int32 [batch], 0 <= seq_lens[b] <= max_seq_len.
+ * seq_lens  device int32 [batch], 0 <= seq_lens[b] <= max_seq_len.  Read
+ *           twice by the score kernel (once to balance valid tiles over the
+ *           SMs before its programmatic-dependent-launch wait, once per
+ *           tile), so it must be complete before the PRECEDING kernel on the
+ *           stream was launched.  No asyncspade kernel writes seq_lens, and a
+ *           kernel that does not trigger PDL (any torch/cuBLAS kernel) runs
+ *           to completion before this call's kernels start, so ordinary
+ *           stream order suffices; only a caller kernel that itself issues
+ *           griddepcontrol.launch_dependents before writing seq_lens breaks
+ *           the rule.
  * sel_idx   device int32 [batch][n_kv_heads][top_k], written.  A row with
  *           seq_lens[b] < top_k holds all its tokens then -1 padding and
  *           sets ASP_FLAG_SHORT_ROW (R13).
@@ -330,6 +339,8 @@ ASP_API asp_status asyncspade_sparse_decode_paged(const asp_decode_params *p, co
  * q         device fp32 [batch][n_q_heads][head_dim] (the current query).
  * sel_idx   device int32 [batch][n_kv_heads][top_k], written.
  * workspace >= asyncspade_quest_select_workspace(p, page_size), 256-B aligned.
+ * Group sizes: G = n_q_heads / n_kv_heads in {1, 2, 4, 8}; others return
+ * ASP_ERR_UNSUPPORTED (and a zero workspace size) before enqueuing anything.
  * Precision: fp32 FMA of the exact bf16 extremes (the bound is exact to
  * ~1e-6 relative); deterministic per row.
  * ---------------------------------------------------------------------- */

@@ -238,8 +238,15 @@ asp_status asyncspade_quest_summarize(const asp_select_params *p, int32_t page_s
                                                 (cudaStream_t)stream));
 }
 
+// the Quest page-bound kernel is instantiated for G in {1, 2, 4, 8} only
+static bool quest_group_ok(const asp_select_params *p) {
+    const int G = p->n_q_heads / p->n_kv_heads;
+    return G == 1 || G == 2 || G == 4 || G == 8;
+}
+
 size_t asyncspade_quest_select_workspace(const asp_select_params *p, int32_t page_size) {
-    if (check_select(p) != ASP_OK || page_size < 1 || page_size > 128 || p->top_k % page_size)
+    if (check_select(p) != ASP_OK || !quest_group_ok(p) || page_size < 1 || page_size > 128 ||
+        p->top_k % page_size)
         return 0;
     return align256(asp_quest_workspace_bytes(*p, page_size));
 }
@@ -250,7 +257,7 @@ asp_status asyncspade_quest_select(const asp_select_params *p, int32_t page_size
                                    asp_stream stream) {
     asp_status st = check_select(p);
     if (st != ASP_OK) return st;
-    if (page_size < 1 || page_size > 128) return ASP_ERR_UNSUPPORTED;
+    if (page_size < 1 || page_size > 128 || !quest_group_ok(p)) return ASP_ERR_UNSUPPORTED;
     if (p->top_k % page_size) return ASP_ERR_SHAPE;
     if (!q || !meta || !seq_lens || !sel_idx) return ASP_ERR_INVALID_ARGUMENT;
     if (!aligned16(q) || !aligned16(meta)) return ASP_ERR_INVALID_ARGUMENT;

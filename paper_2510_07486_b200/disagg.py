@@ -66,7 +66,7 @@ class CacheRank:
         B = st.q.shape[0]
         self.q_t = torch.empty(B, st.n_q, cfg.head_dim, dtype=torch.float32, device=st.device)
         self.kv_t = torch.empty(2, B, st.n_kv, cfg.head_dim, dtype=torch.bfloat16, device=st.device)
-        self.pos = torch.full((B,), cfg.seq_len - 1, dtype=torch.int32, device=st.device)
+        self.pos = torch.sub(st.seq_lens, 1)       # the newest slot (lengths held fixed)
         self.k_sel = torch.empty(B, st.n_kv, cfg.top_k, cfg.head_dim, dtype=torch.bfloat16,
                                  device=st.device)
         self.v_sel = torch.empty_like(self.k_sel)

@@ -46,10 +46,21 @@ class AsyncPipeline:
         self.weights = (torch.zeros(forward_bytes, dtype=torch.uint8, device=dev)
                         if forward_bytes > 0 else None)
         self.sink = torch.zeros(1, dtype=torch.float32, device=dev)
-        self.pos = torch.full((step.cfg.batch * step.layers,), step.cfg.seq_len - 1,
-                              dtype=torch.int32, device=dev)
+        # the fresh token's K/V land at seq_lens[b] - 1: lengths are held fixed
+        # (the steady state), so the newest slot is overwritten each step and
+        # decode's n_fresh = 1 tail attends exactly the pushed row
+        self.pos = torch.empty_like(step.seq_lens)
+        self.set_seq_lens(None)
         self.t = 0
         self.primed = False
+
+    def set_seq_lens(self, lens) -> None:
+        """Set the step's sequence lengths (None: keep them) and the push
+        position seq_lens - 1 that goes with them (plumbing, not per step)."""
+        s = self.step
+        if lens is not None:
+            s.seq_lens.copy_(torch.as_tensor(lens, dtype=torch.int32))
+        torch.sub(s.seq_lens, 1, out=self.pos)
 
     # ------------------------------------------------------------------ pieces
     def select(self, buf: int, stream) -> None:
@@ -71,7 +82,7 @@ class AsyncPipeline:
     def push(self, q_t=None, kv_t=None) -> None:
         """a0 on the current stream, one kernel (asyncspade_append): q_t into the
         window ring and (bf16) the current query, the new token's K/V rows into
-        the newest cache slot (len - 1; lengths are held fixed)."""
+        the newest cache slot (seq_lens[b] - 1; lengths are held fixed)."""
         s = self.step
         if q_t is not None:
             if kv_t is not None:

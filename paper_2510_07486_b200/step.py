@@ -61,7 +61,14 @@ class DecodeStep:
                                   device=dev)
         self.ws_dec = torch.empty(max(sparse_decode_workspace(self.p_dec), 256),
                                   dtype=torch.uint8, device=dev)
-        self.graph = None
+        # one CUDA graph per ring position: the predict launch bakes ring_start
+        # into its parameters, so append() (which advances it) selects another
+        # graph instead of replaying a stale one
+        self.graphs: dict[int, torch.cuda.CUDAGraph] = {}
+
+    @property
+    def graph(self):
+        return self.graphs.get(self.ring_start)
 
     # ------------------------------------------------------------------ inputs
     def fill_synthetic(self, seed: int | None = None) -> None:
@@ -98,7 +105,10 @@ class DecodeStep:
                       out=self.out, workspace=self.ws_dec, stream=stream, params=self.p_dec)
 
     def capture(self) -> torch.cuda.CUDAGraph:
-        """Record run() once into a CUDA graph (warm-up launch first)."""
+        """Record run() into a CUDA graph for the current ring position
+        (warm-up launch first).  Buffers are fixed, so a graph stays valid
+        across fill_synthetic() / append(); append() moves to the graph of
+        the next ring position (captured on first use)."""
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
@@ -107,13 +117,14 @@ class DecodeStep:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             self.run()
-        self.graph = g
+        self.graphs[self.ring_start] = g
         return g
 
     def replay(self) -> None:
-        if self.graph is None:
-            self.capture()
-        self.graph.replay()
+        g = self.graph
+        if g is None:
+            g = self.capture()
+        g.replay()
 
     # ------------------------------------------------------------------ a0: window push
     def append(self, q_t: torch.Tensor, k_new: torch.Tensor | None = None,

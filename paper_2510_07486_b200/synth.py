@@ -129,6 +129,78 @@ def query_trace(seed: int, batch: int, n_q_heads: int, window: int, head_dim: in
     return np.ascontiguousarray(qs[:, :, :window]), f32_to_bf16_bits(qs[:, :, window])
 
 
+# --------------------------------------------------------------------------- structured keys
+# SURVEY §8(d) structured variants (test inputs only): heavy-hitter "needles"
+# and an attention "sink", planted along the newest window query of
+# the KV head's first q head, so they are known at generation time.
+STREAM_NEEDLE = 4
+N_NEEDLES = 32
+NEEDLE_GAIN = 4.0        # needle rows: K += 4 sqrt(D) unit(Q_t)
+SINK_GAIN = 8.0          # token 0:     K += 8 sqrt(D) unit(Q_t)
+
+
+def needle_positions(seed: int, b: int, h: int, seq_len: int, n: int = N_NEEDLES) -> np.ndarray:
+    """n distinct sorted positions in [1, seq_len) for GLOBAL (b, h): a
+    counter-based draw (splitmix64 of (b, h, i)), duplicates skipped."""
+    n = min(n, max(seq_len - 1, 0))
+    key = stream_key(seed, STREAM_NEEDLE)
+    out, seen, i = [], set(), 0
+    while len(out) < n:
+        z = _splitmix64_scalar((key + ((b * 65536 + h) << 20) + i) & M64)
+        t = 1 + int(z % (seq_len - 1))
+        if t not in seen:
+            seen.add(t)
+            out.append(t)
+        i += 1
+    return np.array(sorted(out), np.int64)
+
+
+def structure_direction(seed: int, b: int, h: int, group: int, n_q_heads: int, window: int,
+                        head_dim: int) -> np.ndarray:
+    """fp32 [D]: sqrt(D) * unit(Q_t) for the newest window query of q head h*G
+    (GLOBAL indices), the direction the needles and the sink are planted along."""
+    win, _ = query_trace(seed, b + 1, n_q_heads, window, head_dim, b0=b, h0=h * group,
+                         batch_slice=1, head_slice=1)
+    qt = win[0, 0, window - 1].astype(np.float64)
+    return (np.sqrt(head_dim) * qt / np.linalg.norm(qt)).astype(np.float32)
+
+
+def structured_kv_rows(seed: int, b: int, h: int, seq_len: int, n_kv_heads: int, max_len: int,
+                       head_dim: int, group: int, n_q_heads: int, window: int) -> np.ndarray:
+    """K bf16 bits [seq_len, D] of GLOBAL (b, h) with the needles and the sink
+    planted: row = bf16(float(row) + gain * direction) in fp32 (one RN add,
+    then RNE -- what apply_structure_device does on the GPU)."""
+    K = kv_rows(seed, STREAM_K, b, h, 0, max_len, n_kv_heads, max_len, head_dim)
+    u = structure_direction(seed, b, h, group, n_q_heads, window, head_dim)
+    rows = [(t, np.float32(NEEDLE_GAIN)) for t in needle_positions(seed, b, h, seq_len)]
+    rows.append((0, np.float32(SINK_GAIN)))
+    for t, gain in rows:
+        d = (gain * u).astype(np.float32)
+        K[t] = f32_to_bf16_bits((bf16_bits_to_f32(K[t]) + d).astype(np.float32))
+    return K
+
+
+def apply_structure_device(k_cache, seed: int, seq_len: int, n_kv_heads: int, group: int,
+                           n_q_heads: int, window: int, b0: int = 0, h0: int = 0) -> None:
+    """Plant the needles and the sink into a device K cache view [B_s, H_s, L, D]
+    holding kv_cache(...) values of global (b0.., h0..), exactly as
+    structured_kv_rows does on the host (directions computed on the host)."""
+    import torch
+    B, H, L, D = k_cache.shape
+    for i in range(B):
+        for j in range(H):
+            b, h = b0 + i, h0 + j
+            u = structure_direction(seed, b, h, group, n_q_heads, window, D)
+            pos = needle_positions(seed, b, h, seq_len)
+            d_needle = torch.from_numpy((np.float32(NEEDLE_GAIN) * u).astype(np.float32))
+            d_sink = torch.from_numpy((np.float32(SINK_GAIN) * u).astype(np.float32))
+            dev = k_cache.device
+            p = torch.from_numpy(pos).to(dev)
+            rows = k_cache[i, j].index_select(0, p).float() + d_needle.to(dev)
+            k_cache[i, j].index_copy_(0, p, rows.to(torch.bfloat16))
+            k_cache[i, j, 0] = (k_cache[i, j, 0].float() + d_sink.to(dev)).to(torch.bfloat16)
+
+
 # --------------------------------------------------------------------------- device side
 _synth_lib = None
 

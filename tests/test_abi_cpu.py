@@ -172,3 +172,16 @@ def test_predict_bf16_window_validation(L):
     assert call(1, asp.WINDOW_BF16) == 3
     assert call(8, asp.WINDOW_BF16 | asp.ASSEMBLY_PER_WINDOW) == 3
     assert call(8, asp.WINDOW_BF16 | (1 << 12)) == 1                 # unknown bit
+
+
+def test_quest_group_validation(L):
+    """The Quest comparator is built for G in {1, 2, 4, 8}: larger groups are
+    refused on the host (ASP_ERR_UNSUPPORTED, zero workspace) -- the validation
+    happens before anything could be enqueued."""
+    ok = _sel(n_q_heads=64, top_k=64)                         # G = 8
+    assert L.asyncspade_quest_select_workspace(ctypes.byref(ok), 16) > 0
+    for G in (16, 32):
+        p = _sel(n_q_heads=8 * G, top_k=64)
+        assert L.asyncspade_quest_select_workspace(ctypes.byref(p), 16) == 0
+        assert L.asyncspade_quest_select(ctypes.byref(p), 16, FAKE, FAKE, FAKE, FAKE, FAKE,
+                                         1 << 40, None, None) == 3

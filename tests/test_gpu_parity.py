@@ -256,9 +256,13 @@ def test_decode_edge_cases():
 
 
 # ----------------------------------------------------------------------------- composed step
-def _oracle_row_checks(step: DecodeStep, rows, n_fresh=0, lens=None):
+def _oracle_row_checks(step: DecodeStep, rows, n_fresh=0, lens=None, overlap=None, kv_rows=None):
     """For sampled (b, h): predict / select (band) / decode parity, chained
-    (lens: per-batch sequence lengths of a ragged step; default uniform L)."""
+    (lens: per-batch sequence lengths of a ragged step; default uniform L).
+    overlap (a list): also run the UNCHAINED oracle step (oracle q_hat ->
+    oracle scores -> oracle top-k) and append each row's Eq. 1 overlap ratio
+    |S_gpu & S_oracle| / k.  kv_rows(b, h) ->
+    (K, V) bf16 bits [L, D] overrides the plain generator (structured keys)."""
     cfg = step.cfg
     G, D, L, k, W = cfg.group, cfg.head_dim, cfg.seq_len, cfg.top_k, cfg.window
     seed = synth.base_seed(cfg.index)
@@ -273,11 +277,19 @@ def _oracle_row_checks(step: DecodeStep, rows, n_fresh=0, lens=None):
                                    batch_slice=1, head_slice=G)
         qh_or, _ = oracle.predict(win, step.eps, step.flags)
         assert rel_inf_err(qh_g[b, hl * G:(hl + 1) * G], qh_or[0]) <= Q_HAT_RTOL
-        K = synth.kv_rows(seed, synth.STREAM_K, b, hg, 0, L, cfg.n_kv_heads, L, D)[None, None]
-        V = synth.kv_rows(seed, synth.STREAM_V, b, hg, 0, L, cfg.n_kv_heads, L, D)[None, None]
+        if kv_rows is None:
+            K = synth.kv_rows(seed, synth.STREAM_K, b, hg, 0, L, cfg.n_kv_heads, L, D)[None, None]
+            V = synth.kv_rows(seed, synth.STREAM_V, b, hg, 0, L, cfg.n_kv_heads, L, D)[None, None]
+        else:
+            K, V = (x[None, None] for x in kv_rows(b, hg))
         n = L if lens is None else int(lens[b])
         s_or, _ = oracle.score(qh_g[b:b + 1, hl * G:(hl + 1) * G], K, [n])   # chained
         bands += check_selection(idx_g[b, hl], s_or[0, 0], n - n_fresh, k)["band"]
+        if overlap is not None:                                              # unchained
+            s_un, _ = oracle.score(qh_or, K, [n])
+            i_un, _ = oracle.select(s_un, k, [[n]])
+            a, c = idx_g[b, hl], i_un[0, 0]
+            overlap.append(len(np.intersect1d(a[a >= 0], c[c >= 0])) / max(min(k, n), 1))
         o_or = oracle.sparse_decode(q, K, V, idx_g[b:b + 1, hl:hl + 1], [n], n_fresh)
         assert rel_inf_err(out_g[b, hl * G:(hl + 1) * G], o_or[0]) <= ATTN_RTOL
     return bands
@@ -297,7 +309,10 @@ def test_step_qwen3_8b_sampled_rows():
     step.run()
     torch.cuda.synchronize()
     assert int(step.dev_flags.item()) == 0
-    _oracle_row_checks(step, rows_sample(step.cfg.batch * step.n_kv, 12, seed=1))
+    ov = []
+    _oracle_row_checks(step, rows_sample(step.cfg.batch * step.n_kv, 32, seed=1), overlap=ov)
+    # unchained end to end (oracle q_hat): Eq. 1 overlap >= 0.999
+    assert np.mean(ov) >= 0.999 and min(ov) >= 0.99, (np.mean(ov), min(ov))
     del step
     torch.cuda.empty_cache()
 
@@ -314,7 +329,11 @@ def test_step_qwen3_32b_graph_sampled_rows_and_determinism():
     step.replay()
     torch.cuda.synchronize()
     assert torch.equal(idx1, step.sel_idx) and torch.equal(out1, step.out)
-    _oracle_row_checks(step, rows_sample(step.cfg.batch * step.n_kv, 8, seed=2))
+    # the deterministic 32-row subset of SURVEY §8(d) / BASELINE.md §3, chained
+    # parity on each, and the unchained Eq. 1 overlap ratio
+    ov = []
+    _oracle_row_checks(step, rows_sample(step.cfg.batch * step.n_kv, 32, seed=2), overlap=ov)
+    assert np.mean(ov) >= 0.999 and min(ov) >= 0.99, (np.mean(ov), min(ov))
     del step
     torch.cuda.empty_cache()
 
@@ -646,12 +665,12 @@ def test_dual_rank_disaggregation_matches_single_rank_pipeline():
     """NEXT-1: an Inference Rank and a Cache Rank (two processes
     on one GPU, gloo with host staging) exchanging packs and selected K/V
     rows produce, step for step, bit for bit the single-rank a5 pipeline's
-    output on the same inputs (scripts/exp_disagg_gloo.py runs both ranks and
+    output on the same inputs (scripts/disagg_two_rank.py runs both ranks and
     the reference; it prints one line per step)."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "exp_disagg_gloo.py")],
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "disagg_two_rank.py")],
                        capture_output=True, text=True, timeout=300, cwd=root)
     lines = [ln for ln in r.stdout.splitlines() if " out eq " in ln]
     assert r.returncode == 0 and len(lines) == 3, r.stdout[-2000:] + r.stderr[-2000:]

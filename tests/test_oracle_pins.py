@@ -474,3 +474,66 @@ def test_quest_short_rows_and_partial_last_page():
     idx, pidx, _ = oracle.quest_select(q, K, [20], 48, 16)     # 2 pages exist, 3 wanted
     assert list(pidx[0, 0]) == [0, 1, -1]
     np.testing.assert_array_equal(idx[0, 0], np.r_[np.arange(20), -np.ones(28, int)])
+
+
+def test_select_signed_zero_ties_and_nan_fill():
+    """R14 + R9, pinned independently of the oracle's own code: -0.0 and +0.0
+    are EQUAL numbers (IEEE 754 5.11), so they tie and the lower index wins
+    whichever sign it carries; NaNs rank below every number and fill a row
+    that has fewer than k numbers in index order (the brute-force
+    lexicographic sort with NaN mapped below -inf)."""
+    cases = [
+        (np.array([-1.0, -0.0, 0.0, -0.0, 2.0]), 3, [1, 2, 4]),
+        (np.array([0.0, -0.0]), 1, [0]),
+        (np.array([-0.0, 0.0]), 1, [0]),
+        (np.array([-0.0, -5.0, 0.0, 0.0]), 2, [0, 2]),
+        (np.array([np.nan, 1.0, np.nan, np.nan]), 3, [0, 1, 2]),
+        (np.array([np.nan, -np.inf, np.nan]), 2, [0, 1]),
+    ]
+    for s, k, exp in cases:
+        idx, cond = oracle.select(s, k)
+        np.testing.assert_array_equal(idx, exp)
+        assert bool(cond & oracle.FLAG_NONFINITE) == bool(np.isnan(s).any())
+        key = np.where(np.isnan(s), -np.inf, s)          # brute force, NaN below everything
+        order = np.lexsort((np.arange(len(s)), np.isnan(s), -key))
+        np.testing.assert_array_equal(np.sort(order[:k]), exp)
+    # a random row salted with signed zeros and NaNs against the brute force
+    rng = np.random.default_rng(41)
+    s = rng.integers(-3, 4, 500).astype(np.float64)
+    s[rng.random(500) < 0.3] = -0.0
+    s[rng.random(500) < 0.05] = np.nan
+    idx, _ = oracle.select(s, 300)
+    key = np.where(np.isnan(s), -np.inf, s)
+    order = np.lexsort((np.arange(500), np.isnan(s), -key))
+    np.testing.assert_array_equal(idx, np.sort(order[:300]))
+
+
+def test_ar1_prediction_beats_random_selection():
+    """SPEC S:712-713 sanity check (SURVEY §8(c) 'end-to-end sanity'): on
+    SPEC's AR(1) query traces (alpha 0.95) the selection made with the
+    predicted query q_hat overlaps the selection of the TRUE next query
+    q_{t+1} (Eq. 1) at least 3x as much as a random selection
+    (k/N = 1/8).  Keys ~ N(0,1), N = 2048, k = 256, W = 16."""
+    rng = np.random.default_rng(2025)
+    B, Hq, W, D, N, k = 4, 8, 16, 64, 2048, 256
+    T = W + 1
+    q = np.empty((B, Hq, T, D))
+    q[:, :, 0] = rng.standard_normal((B, Hq, D))
+    for t in range(1, T):
+        q[:, :, t] = 0.95 * q[:, :, t - 1] + 0.05 * rng.standard_normal((B, Hq, D))
+    win = q[:, :, :W].astype(np.float32)
+    nxt = q[:, :, W].astype(np.float32)
+    K = synth.f32_to_bf16_bits(rng.standard_normal((B, Hq, N, D)).astype(np.float32))
+    qh, cond = oracle.predict(win)
+    assert cond == 0
+    s_hat, _ = oracle.score(qh, K, [N] * B)
+    s_true, _ = oracle.score(nxt, K, [N] * B)
+    i_hat, _ = oracle.select(s_hat, k)
+    i_true, _ = oracle.select(s_true, k)
+    ov = np.mean([len(np.intersect1d(i_hat[b, h], i_true[b, h])) / k
+                  for b in range(B) for h in range(Hq)])
+    assert ov >= 3 * k / N, ov
+    # and a random index set really sits near k / N (the baseline is meaningful)
+    rnd = np.mean([len(np.intersect1d(np.sort(rng.choice(N, k, replace=False)), i_true[b, h])) / k
+                   for b in range(B) for h in range(Hq)])
+    assert abs(rnd - k / N) < 0.03, rnd

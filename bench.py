@@ -36,8 +36,9 @@ UNIT = "us/step"
 def _args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=300,
+                    help="timed steps (default 300: >= 200 ms of CUDA-graph replays at config [2])")
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="asyncspade", choices=["asyncspade", "reference"])
     ap.add_argument("--config", default="qwen3-32b_b64_ctx32k")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -57,7 +58,67 @@ def _args():
                          "placement) through the *_paged entry points (SURVEY §8(f) NEXT-4)")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: skip clocks, e2e and the CPU baseline")
+    ap.add_argument("--eager", action="store_true",
+                    help="time eager back-to-back launches instead of CUDA-graph replays")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="multi-rank plumbing only (no kernels; gloo on CPU): every rank "
+                         "reports its shard, rank 0 prints one JSON line")
     return ap.parse_args()
+
+
+def _self_launch(args) -> None:
+    """`bench.py --gpus N` (N > 1) outside torchrun: re-exec under
+    torch.distributed.run with one rank per GPU (127.0.0.1 rendezvous)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def launch_check(args, cfg) -> None:
+    """The multi-rank plumbing of the GPU arm without kernels: rendezvous,
+    the §8(e) partition (shard_units), a MAX all-reduce of per-rank times and
+    the head-major output gather, on gloo (CPU) or NCCL."""
+    import torch
+    import torch.distributed as dist
+    from paper_2510_07486_b200 import shard as sh_mod
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        dist.init_process_group("gloo")
+    sh = sh_mod.shard_units(cfg.batch, cfg.n_kv_heads, world, rank)
+    q0, qn = sh.q_heads(cfg.group)
+    # a stand-in output block: value = global (q head, batch) id, head-major
+    hq = torch.arange(q0, q0 + qn, dtype=torch.float64)[:, None]
+    bb = torch.arange(sh.b0, sh.b0 + sh.bn, dtype=torch.float64)[None, :]
+    blk = (hq * cfg.batch + bb).contiguous()
+    t = torch.tensor([1.0 + rank], dtype=torch.float64)
+    if world > 1:
+        full = sh_mod.gather_units(blk, sh, cfg.batch, cfg.n_q_heads, cfg.group)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        shards = [None] * world
+        dist.all_gather_object(shards, [sh.b0, sh.bn, sh.h0, sh.hn])
+    else:
+        full, shards = blk, [[sh.b0, sh.bn, sh.h0, sh.hn]]
+    ok = bool(torch.equal(full, torch.arange(cfg.n_q_heads * cfg.batch,
+                                             dtype=torch.float64).view(cfg.n_q_heads, cfg.batch)))
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": world, "config": cfg.name,
+                          "shards_b0_bn_h0_hn": shards, "max_over_ranks": float(t[0]),
+                          "gather_ok": ok}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def _peaks():
@@ -133,8 +194,27 @@ class Clocks:
 
 
 # --------------------------------------------------------------------------- reference arm
+# The oracle as it stands (plain C, one thread per call), run on every host
+# core at once: one worker process per core, each owning a few (batch,
+# kv-head) rows whose inputs it generates BEFORE the timed region (generation
+# is not the oracle).  A timed "round" = every worker runs the full oracle
+# step (c1 -> c2 -> c3 -> c4) on one of its rows; its wall time is
+# max(end) - min(start) over the workers (CLOCK_MONOTONIC, shared by the
+# processes).  Scaled to the workload's row count.
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def _oracle_rows(cfg, rows, seed):
-    """Host inputs for sampled (b, kv-head) rows (generation excluded from timing)."""
+    """Host inputs for (b, kv-head) rows (generation excluded from timing)."""
     from paper_2510_07486_b200 import synth
     G, D, L = cfg.group, cfg.head_dim, cfg.seq_len
     data = []
@@ -148,49 +228,118 @@ def _oracle_rows(cfg, rows, seed):
     return data
 
 
-def _oracle_time(cfg, data):
-    """Wall time of the oracle's full step (c1 -> c2 -> c3 -> c4) over the rows."""
+def _oracle_worker(cfg_name, rows, seed, cmd_q, res_q):
+    sys.path.insert(0, ROOT)
     import oracle
+    from paper_2510_07486_b200 import configs
+    cfg = configs.by_name(cfg_name)
+    data = _oracle_rows(cfg, rows, seed)
+    oracle.build()
+    res_q.put(("ready", None, None))
+    while True:
+        i = cmd_q.get()
+        if i is None:
+            return
+        win, q, K, V = data[i % len(data)]
+        t0 = time.perf_counter()
+        oracle.step(win, q, K, V, [cfg.seq_len], cfg.top_k)
+        res_q.put(("done", t0, time.perf_counter()))
+
+
+class OraclePool:
+    """One oracle worker process per host core (os.sched_getaffinity)."""
+
+    def __init__(self, cfg, rows_per_worker: int, cores: int | None = None, seed=None):
+        import multiprocessing as mp
+        from paper_2510_07486_b200 import synth
+        self.cfg = cfg
+        self.cores = cores or len(os.sched_getaffinity(0))
+        n_rows = cfg.batch * cfg.n_kv_heads
+        seed = synth.base_seed(cfg.index) if seed is None else seed
+        ctx = mp.get_context("spawn")
+        self.res_q = ctx.Queue()
+        self.cmd_qs, self.procs = [], []
+        for w in range(self.cores):
+            rows = [((w * rows_per_worker + j) * 37) % n_rows for j in range(rows_per_worker)]
+            cq = ctx.Queue()
+            pr = ctx.Process(target=_oracle_worker, args=(cfg.name, rows, seed, cq, self.res_q),
+                             daemon=True)
+            pr.start()
+            self.cmd_qs.append(cq)
+            self.procs.append(pr)
+        for _ in range(self.cores):
+            self.res_q.get(timeout=600)
+
+    def round(self, i: int) -> float:
+        """Every worker runs the full oracle step on its i-th row; wall seconds."""
+        for cq in self.cmd_qs:
+            cq.put(i)
+        ts = [self.res_q.get(timeout=600) for _ in self.cmd_qs]
+        return max(t[2] for t in ts) - min(t[1] for t in ts)
+
+    def close(self):
+        for cq in self.cmd_qs:
+            cq.put(None)
+        for pr in self.procs:
+            pr.join(timeout=10)
+
+
+def _single_thread_us_per_row(cfg, n_rows: int = 8) -> float:
+    """One thread, the oracle's full step on a fixed n-row subset."""
+    import oracle
+    from paper_2510_07486_b200 import synth
+    total = cfg.batch * cfg.n_kv_heads
+    rows = [int(i * total / min(n_rows, total)) for i in range(min(n_rows, total))]
+    data = _oracle_rows(cfg, rows, synth.base_seed(cfg.index))
     t0 = time.perf_counter()
     for win, q, K, V in data:
         oracle.step(win, q, K, V, [cfg.seq_len], cfg.top_k)
-    return time.perf_counter() - t0
+    return (time.perf_counter() - t0) / len(rows) * 1e6
 
 
-def cpu_baseline(cfg, target_s: float = 12.0):
-    """The oracle, as it stands (one thread), on a bounded sample of rows."""
-    from paper_2510_07486_b200 import synth
-    seed = synth.base_seed(cfg.index)
+def cpu_baseline(cfg, target_rounds: int = 4):
+    """The oracle, as it stands, on all host cores: `target_rounds` rounds of
+    one row per core (a bounded sample of the workload), scaled to a whole
+    step; plus the one-thread time of configs [0] and [1] on 8 rows."""
+    from paper_2510_07486_b200 import configs
+    pool = OraclePool(cfg, rows_per_worker=target_rounds)
+    try:
+        pool.round(0)                                            # warm (page-in, caches)
+        walls = [pool.round(i) for i in range(target_rounds)]
+    finally:
+        pool.close()
+    rows_done = pool.cores * target_rounds
     n_rows_total = cfg.batch * cfg.n_kv_heads
-    probe = _oracle_rows(cfg, [0], seed)
-    t1 = _oracle_time(cfg, probe)
-    n = max(1, min(n_rows_total, int(target_s / max(t1, 1e-3))))
-    rows = [int(i * n_rows_total / n) for i in range(n)]
-    data = _oracle_rows(cfg, rows, seed)
-    t = _oracle_time(cfg, data)
-    us_per_step = t / n * n_rows_total * 1e6
-    return {"value": us_per_step, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{n} of {n_rows_total} (batch, kv-head) rows of {cfg.name}, full step "
-                      f"(predict, fp64 score, full sort, fp64 decode), scaled to a whole step; "
-                      f"{t:.1f} s wall"}
+    wall = sum(walls)
+    us_per_step = wall / rows_done * n_rows_total * 1e6
+    single = {c.name: _single_thread_us_per_row(c) * c.batch * c.n_kv_heads
+              for c in (configs.TINY, configs.QWEN3_8B)}
+    return {"value": us_per_step, "unit": UNIT, "cores": pool.cores, "kind": "oracle",
+            "cpu_model": _cpu_model(),
+            "sample": f"{rows_done} of {n_rows_total} (batch, kv-head) rows of {cfg.name} "
+                      f"({target_rounds} rounds x {pool.cores} worker processes, one row each), "
+                      f"full oracle step (fp64 predict, fp64 score, full sort, fp64 decode), "
+                      f"scaled to a whole step; {wall:.2f} s wall",
+            "single_thread_us_per_step": single,
+            "single_thread_sample": "8 fixed rows (all rows of the tiny config), one thread, "
+                                    "scaled to the config's whole step"}
 
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2510_07486_b200 import synth
-    seed = synth.base_seed(cfg.index)
     n_rows_total = cfg.batch * cfg.n_kv_heads
-    rows_per_step = 4
-    times = []
-    for i in range(args.warmup + args.steps):
-        rows = [(i * rows_per_step + j) * 37 % n_rows_total for j in range(rows_per_step)]
-        data = _oracle_rows(cfg, rows, seed)
-        t = _oracle_time(cfg, data)
-        if i >= args.warmup:
-            times.append(t / rows_per_step * n_rows_total * 1e6)
-    v = statistics.mean(times)
+    pool = OraclePool(cfg, rows_per_worker=4)
+    try:
+        for i in range(args.warmup):
+            pool.round(i)
+        per_row = []
+        for i in range(args.steps):
+            per_row.append(pool.round(i) / pool.cores)
+    finally:
+        pool.close()
+    v = statistics.mean(per_row) * n_rows_total * 1e6
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": v / 1e3, "higher_is_better": False, "scaling": "strong",
@@ -198,9 +347,11 @@ def run_reference(args, cfg):
             "config": {"workload": cfg.name, "batch": cfg.batch, "n_q_heads": cfg.n_q_heads,
                        "n_kv_heads": cfg.n_kv_heads, "head_dim": cfg.head_dim,
                        "seq_len": cfg.seq_len, "top_k": cfg.top_k, "window": cfg.window},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{rows_per_step} of {n_rows_total} (batch, kv-head) rows "
-                                       "per step, full oracle step, scaled to a whole step"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": pool.cores, "kind": "oracle",
+                             "cpu_model": _cpu_model(),
+                             "sample": f"per step: {pool.cores} of {n_rows_total} (batch, kv-head) "
+                                       f"rows, one per core (worker process), full oracle step, "
+                                       f"scaled to a whole step"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -210,6 +361,9 @@ def main():
     args = _args()
     from paper_2510_07486_b200 import configs
     cfg = configs.by_name(args.config)
+    _self_launch(args)
+    if args.launch_check:
+        return launch_check(args, cfg)
     if args.impl == "reference":
         return run_reference(args, cfg)
 
@@ -227,17 +381,20 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2510_07486_b200.shard import kv_head_shard
+    from paper_2510_07486_b200.shard import shard_units
     shards = args.emulate_shard if (args.emulate_shard and world == 1) else world
-    h0, hn = kv_head_shard(cfg.n_kv_heads, shards, rank)    # §8(e): KV-head sharding
+    sh = shard_units(cfg.batch, cfg.n_kv_heads, shards, rank)   # §8(e): KV heads, then batch
+    h0, hn = sh.h0, sh.hn
     wdt = torch.bfloat16 if args.bf16_window else torch.float32
-    step = DecodeStep(cfg, "cuda", kv_heads=(h0, hn), window_dtype=wdt)
+    step = DecodeStep(cfg, "cuda", kv_heads=(h0, hn), window_dtype=wdt,
+                      batch_range=(sh.b0, sh.bn))
     step.fill_synthetic()
-    lens = [cfg.seq_len] * cfg.batch
+    lens = [cfg.seq_len] * sh.bn
     if args.ragged:
         import numpy as np
         rng = np.random.default_rng(synth.base_seed(cfg.index) + 99)
         lens = [int(x) for x in rng.integers(cfg.seq_len // 8, cfg.seq_len + 1, cfg.batch)]
+        lens = lens[sh.b0:sh.b0 + sh.bn]
         step.seq_lens.copy_(torch.tensor(lens, dtype=torch.int32))
     torch.cuda.synchronize()
 
@@ -298,30 +455,79 @@ def main():
     for _ in range(max(args.warmup, 1)):
         one_step()
     barrier()
-    # (1) the headline: K back-to-back steps, device events only around the
-    #     whole region (events between the calls would break the programmatic
-    #     dependent launch overlap of consecutive kernels)
+    # (1) the headline: K steps replayed from CUDA graphs; a
+    #     graph holds `per_graph` consecutive steps, so the programmatic
+    #     dependent launch edges between one step's last kernel and the next
+    #     step's first are kept inside it; device events only around the
+    #     whole region.  --eager: the same K steps as eager launches.
+    per_graph = 1 if args.eager else min(10, args.steps)
+    graphs = {}
+
+    def graph_of(n):
+        if n not in graphs:
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                one_step()                       # warm the side stream's first launch
+            stream.wait_stream(side)
+            with torch.cuda.graph(g):
+                for _ in range(n):
+                    one_step()
+            graphs[n] = g
+        return graphs[n]
+
+    def run_steps(k):
+        if args.eager:
+            for _ in range(k):
+                one_step()
+            return
+        full, rest = divmod(k, per_graph)
+        for _ in range(full):
+            graph_of(per_graph).replay()
+        if rest:
+            graph_of(rest).replay()
+
+    if not args.eager:
+        graph_of(per_graph)
+        if args.steps % per_graph:
+            graph_of(args.steps % per_graph)
+        run_steps(per_graph)
+        barrier()
     t0, t1 = ev(), ev()
     with Clocks(local) as clk:
-        for _ in range(2):               # re-warm after the sampler's start-up idle gap
-            one_step()
+        run_steps(2 * per_graph)             # re-warm after the sampler's start-up idle gap
         barrier()
         t0.record(stream)
-        for i in range(args.steps):
-            one_step()
+        run_steps(args.steps)
         t1.record(stream)
         barrier()
     ms_step = t0.elapsed_time(t1) / args.steps
+    # per-replay distribution (graphs of `per_graph` steps, events between replays)
+    rep_us = []
+    if not args.eager:
+        evs_r = [ev() for _ in range(min(args.steps // per_graph, 50) + 1)]
+        barrier()
+        evs_r[0].record(stream)
+        for j in range(1, len(evs_r)):
+            graph_of(per_graph).replay()
+            evs_r[j].record(stream)
+        barrier()
+        rep_us = sorted(evs_r[j - 1].elapsed_time(evs_r[j]) * 1e3 / per_graph
+                        for j in range(1, len(evs_r)))
+    graphs.clear()
     # (2) the per-call breakdown (and the live roofline of score_select):
     #     another K steps with events between the calls
-    events = [[ev() for _ in range(4)] for _ in range(args.steps)]
+    n_brk = min(args.steps, 20)
+    events = [[ev() for _ in range(4)] for _ in range(n_brk)]
     barrier()
-    for i in range(args.steps):
+    for i in range(n_brk):
         one_step(events[i])
     barrier()
     seg = [[e[j].elapsed_time(e[j + 1]) for e in events] for j in range(3)]
     per_step = sorted(e[0].elapsed_time(e[3]) * 1e3 for e in events)
     pct = lambda q: per_step[min(len(per_step) - 1, int(q * (len(per_step) - 1) + 0.5))]
+    rq = lambda q: rep_us[min(len(rep_us) - 1, int(q * (len(rep_us) - 1) + 0.5))]
     avg_pred, avg_sel, avg_dec = (statistics.mean(s) for s in seg)
     t = torch.tensor([ms_step, avg_sel], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -354,7 +560,7 @@ def main():
     # timed region.
     e2e = None
     if not (args.no_e2e or args.profile):
-        B, nq, D = cfg.batch, step.n_q, cfg.head_dim
+        B, nq, D = sh.bn, step.n_q, cfg.head_dim
         L = cfg.seq_len
         h_qt = [torch.randn(B, nq, D, dtype=torch.float32).pin_memory() for _ in range(2)]
         h_kv = [torch.randn(2, B, step.n_kv, D).to(torch.bfloat16).pin_memory() for _ in range(2)]
@@ -362,7 +568,7 @@ def main():
         d_qt = [torch.empty(B, nq, D, dtype=torch.float32, device="cuda") for _ in range(2)]
         d_kv = [torch.empty(2, B, step.n_kv, D, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
         d_out = [torch.empty(B, nq, D, dtype=torch.float32, device="cuda") for _ in range(2)]
-        pos = torch.full((B,), L - 1, dtype=torch.int32, device="cuda")
+        pos = step.seq_lens - 1                              # the newest slot of each row
         copy = torch.cuda.Stream()
         h2d_done = [torch.cuda.Event() for _ in range(2)]
         used = [torch.cuda.Event() for _ in range(2)]
@@ -428,7 +634,8 @@ def main():
         from paper_2510_07486_b200.pipeline import AsyncPipeline
         del step
         torch.cuda.empty_cache()
-        st1 = DecodeStep(cfg, "cuda", kv_heads=(h0, hn), n_fresh=1, window_dtype=wdt)
+        st1 = DecodeStep(cfg, "cuda", kv_heads=(h0, hn), n_fresh=1, window_dtype=wdt,
+                         batch_range=(sh.b0, sh.bn))
         st1.fill_synthetic()
         st1.seq_lens.copy_(torch.tensor(lens, dtype=torch.int32))
         pipe = AsyncPipeline(st1)
@@ -474,8 +681,9 @@ def main():
                                     if args.ragged else "uniform L"),
                        "kv_layout": (f"paged: {args.paged}-token HND pages, random placement"
                                      if args.paged else "dense [B][Hkv][L][D]"),
-                       "parallelism": f"kv-head shard x{world}" if shards == world else
-                                      f"emulated: rank 0 of a {shards}-way kv-head shard on 1 GPU",
+                       "parallelism": (f"kv-head shard x{world}" if shards == world else
+                                       f"emulated: rank 0 of a {shards}-way kv-head shard on 1 GPU")
+                                      + ("" if sh.bn == cfg.batch else " (batch split)"),
                        "l2": "no flush: K+V per GPU (%.2f GB) >> 126 MB L2" %
                              (2 * k_bytes / 1e9)},
             "hbm_tb_per_s": core / (ms_step * 1e-3) / 1e12,
@@ -484,15 +692,20 @@ def main():
             "roofline_frac_step_nominal_8tbs": core / (ms_step * 1e-3) / 8e12,
             "per_call_ms": {"predict_query": avg_pred, "score_select": avg_sel,
                             "sparse_decode": avg_dec},
-            "step_us_p10_p50_p90": [pct(0.1), pct(0.5), pct(0.9)],
+            "step_us_p10_p50_p90": ([rq(0.1), rq(0.5), rq(0.9)] if rep_us else
+                                    [pct(0.1), pct(0.5), pct(0.9)]),
             "roofline": {"bound": "hbm", "kernel": "asyncspade_score_select (score + select)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic(),
                          "algorithmic_bytes_per_launch": k_bytes, "peak_source": peak_src},
             "gpu_launches": 5 * args.steps,
             "gpu_launches_e2e_per_step": 6,
-            "timing": "headline: events around K back-to-back steps; per_call_ms / roofline: a "
-                      "second K-step pass with events between the calls",
+            "timing": (("headline: CUDA-graph replays (%d steps per graph, PDL edges kept "
+                        "inside), events around all K steps (%.0f ms timed); p10/p50/p90 of "
+                        "per-replay times / %d; " % (per_graph, ms_step * args.steps, per_graph))
+                       if not args.eager else "headline: events around K eager back-to-back "
+                       "steps; ") + "per_call_ms / roofline: a second pass of %d eager steps "
+                      "with events between the calls" % n_brk,
             "dev_flags": flags,
             "clocks": clk.summary(),
         }

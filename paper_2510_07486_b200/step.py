@@ -30,7 +30,8 @@ from .configs import Config
 class DecodeStep:
     def __init__(self, cfg: Config, device="cuda", *, kv_heads: tuple[int, int] | None = None,
                  n_fresh: int = 0, eps: float = 1e-2, flags: int = 0, keep_scores: bool = False,
-                 layers: int = 1, window_dtype: torch.dtype = torch.float32):
+                 layers: int = 1, window_dtype: torch.dtype = torch.float32,
+                 batch_range: tuple[int, int] | None = None):
         self.cfg = cfg
         self.layers = layers
         self.device = torch.device(device)
@@ -39,7 +40,9 @@ class DecodeStep:
         G = cfg.group
         self.q0, self.n_q = h0 * G, hn * G
         W, D, L = cfg.window, cfg.head_dim, cfg.seq_len
-        B = cfg.batch * layers                     # layer-major packing along the batch axis
+        # batch rows [b0, b0 + n_b) of the global batch (a batch-split shard, §8(e))
+        self.b0, self.n_b = batch_range if batch_range is not None else (0, cfg.batch)
+        B = self.n_b * layers                      # layer-major packing along the batch axis
         dev = self.device
         self.n_fresh, self.eps, self.flags = n_fresh, eps, flags
         self.ring_start = 0
@@ -76,19 +79,21 @@ class DecodeStep:
         values of global heads [h0, h0+n) -- identical on any sharding."""
         cfg = self.cfg
         seed = synth.base_seed(cfg.index) if seed is None else seed
-        B = cfg.batch
+        B = self.n_b
         for layer in range(self.layers):
             sd = seed + synth.LAYER_SEED_STRIDE * layer
             rows = slice(layer * B, (layer + 1) * B)
-            synth.fill_kv_device(self.k_cache[rows], sd, synth.STREAM_K, 0, self.h0, cfg.n_kv_heads)
-            synth.fill_kv_device(self.v_cache[rows], sd, synth.STREAM_V, 0, self.h0, cfg.n_kv_heads)
+            synth.fill_kv_device(self.k_cache[rows], sd, synth.STREAM_K, self.b0, self.h0,
+                                 cfg.n_kv_heads)
+            synth.fill_kv_device(self.v_cache[rows], sd, synth.STREAM_V, self.b0, self.h0,
+                                 cfg.n_kv_heads)
             if self.window.dtype == torch.float32:
-                synth.fill_query_device(self.window[rows], self.q[rows].view(torch.int16), sd, 0,
-                                        self.q0, cfg.n_q_heads)
+                synth.fill_query_device(self.window[rows], self.q[rows].view(torch.int16), sd,
+                                        self.b0, self.q0, cfg.n_q_heads)
             else:                                          # a bf16 ring: the rounded trace
                 w32 = torch.empty(self.window[rows].shape, dtype=torch.float32, device=self.device)
-                synth.fill_query_device(w32, self.q[rows].view(torch.int16), sd, 0, self.q0,
-                                        cfg.n_q_heads)
+                synth.fill_query_device(w32, self.q[rows].view(torch.int16), sd, self.b0,
+                                        self.q0, cfg.n_q_heads)
                 self.window[rows].copy_(w32)
         self.ring_start = 0
         self.p_pred.ring_start = 0

@@ -26,28 +26,32 @@ def _free_port() -> int:
 CFG = configs.QWEN3_8B.with_(batch=2, seq_len=512, top_k=64, window=8, head_dim=64)
 
 
-def _shard_step(rank: int, world: int):
+# MQA (one KV head): two ranks split the batch
+CFG_MQA = configs.Config("mqa-cpu", 0, 4, 8, 1, 64, 384, 48, 8)
+
+
+def _shard_step(rank: int, world: int, cfg=CFG):
+    """The rank's block of the step (head-major outputs [heads, batch, ...])."""
     import oracle
-    cfg = CFG
     seed = synth.base_seed(cfg.index)
-    h0, hn = shard.kv_head_shard(cfg.n_kv_heads, world, rank)
-    q0, qn = shard.q_head_shard(cfg.n_q_heads, cfg.n_kv_heads, world, rank)
+    sh = shard.shard_units(cfg.batch, cfg.n_kv_heads, world, rank)
+    q0, qn = sh.q_heads(cfg.group)
     win, q = synth.query_trace(seed, cfg.batch, cfg.n_q_heads, cfg.window, cfg.head_dim,
-                               h0=q0, head_slice=qn)
+                               b0=sh.b0, batch_slice=sh.bn, h0=q0, head_slice=qn)
     K = synth.kv_cache(seed, synth.STREAM_K, cfg.batch, cfg.n_kv_heads, cfg.seq_len,
-                       cfg.head_dim, h0=h0, head_slice=hn)
+                       cfg.head_dim, b0=sh.b0, batch_slice=sh.bn, h0=sh.h0, head_slice=sh.hn)
     V = synth.kv_cache(seed, synth.STREAM_V, cfg.batch, cfg.n_kv_heads, cfg.seq_len,
-                       cfg.head_dim, h0=h0, head_slice=hn)
-    _, _, idx, out = oracle.step(win, q, K, V, [cfg.seq_len] * cfg.batch, cfg.top_k)
-    return idx, out
+                       cfg.head_dim, b0=sh.b0, batch_slice=sh.bn, h0=sh.h0, head_slice=sh.hn)
+    _, _, idx, out = oracle.step(win, q, K, V, [cfg.seq_len] * sh.bn, cfg.top_k)
+    return np.ascontiguousarray(idx.transpose(1, 0, 2)), np.ascontiguousarray(out.transpose(1, 0, 2)), sh
 
 
-def _worker(rank, world, port, result_q):
+def _worker(rank, world, port, result_q, cfg=CFG):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    idx, out = _shard_step(rank, world)
-    full_out = shard.gather_heads(torch.from_numpy(out))
-    full_idx = shard.gather_heads(torch.from_numpy(idx))
+    idx, out, sh = _shard_step(rank, world, cfg)
+    full_out = shard.gather_units(torch.from_numpy(out), sh, cfg.batch, cfg.n_q_heads, cfg.group)
+    full_idx = shard.gather_units(torch.from_numpy(idx), sh, cfg.batch, cfg.n_kv_heads, 1)
     if rank == 0:
         result_q.put((full_idx.numpy(), full_out.numpy()))
     dist.barrier()
@@ -55,6 +59,13 @@ def _worker(rank, world, port, result_q):
 
 
 def test_shard_bounds():
+    assert shard.shard_units(64, 8, 8, 3) == shard.Shard(0, 64, 3, 1)
+    # P > Hkv: "by batch where heads run out" -- MQA over 8 ranks, 2 KV heads over 8
+    assert [shard.shard_units(10, 1, 4, r) for r in range(4)] == [
+        shard.Shard(0, 2, 0, 1), shard.Shard(2, 3, 0, 1), shard.Shard(5, 2, 0, 1), shard.Shard(7, 3, 0, 1)]
+    assert shard.shard_units(64, 2, 8, 5) == shard.Shard(16, 16, 1, 1)
+    with pytest.raises(ValueError):
+        shard.shard_units(64, 8, 12, 0)
     assert shard.kv_head_shard(8, 1, 0) == (0, 8)
     assert [shard.kv_head_shard(8, 4, r) for r in range(4)] == [(0, 2), (2, 2), (4, 2), (6, 2)]
     assert shard.q_head_shard(64, 8, 8, 3) == (24, 8)
@@ -62,18 +73,19 @@ def test_shard_bounds():
         shard.kv_head_shard(8, 3, 0)
 
 
-def test_two_rank_gloo_sharded_step_matches_unsharded():
+@pytest.mark.parametrize("cfg", [CFG, CFG_MQA], ids=["kv-head-split", "mqa-batch-split"])
+def test_two_rank_gloo_sharded_step_matches_unsharded(cfg):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, cfg)) for r in range(2)]
     for p in procs:
         p.start()
     idx, out = q.get(timeout=300)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    ref_idx, ref_out = _shard_step(0, 1)
+    ref_idx, ref_out, _ = _shard_step(0, 1, cfg)
     np.testing.assert_array_equal(idx, ref_idx)
     np.testing.assert_array_equal(out, ref_out)
 

@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define ASYNCSPADE_ABI_VERSION 1
+#define ASYNCSPADE_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define ASP_API __attribute__((visibility("default")))
@@ -115,8 +115,11 @@ typedef void *asp_stream;  /* cudaStream_t */
  * ring_start = (ring_slot + 1) % window (the slot written is the newest).
  *
  * q_t       device fp32 [batch][n_q_heads][head_dim].
- * q_window  device fp32 [batch][n_q_heads][window][head_dim] (ring).
- * q_cur     nullable device bf16 [batch][n_q_heads][head_dim].
+ * q_window  device fp32 [batch][n_q_heads][window][head_dim] (ring), or
+ *           null (no predictor state here: the Inference Rank of the
+ *           disaggregated form only needs q_cur and its fresh K / V row).
+ * q_cur     nullable device bf16 [batch][n_q_heads][head_dim]; q_window and
+ *           q_cur cannot both be null.
  * k_new, v_new  nullable device bf16 [batch][n_kv_heads][head_dim].
  * k_cache, v_cache  strided as asp_decode_params' caches (nullable iff the
  *           matching *_new is).  pos nullable device int32 [batch]: the
@@ -228,7 +231,7 @@ ASP_API asp_status asyncspade_score_select(const asp_select_params *p, const flo
  *     out = sum_j softmax_j(sm_scale * q . K_j) V_j
  * with fp32 logits (bf16 x bf16 products are exact), fp32 softmax and fp32
  * accumulation, split over fixed 256-entry chunks of the selection merged
- * in a fixed order.  An empty set gives out = 0.
+ * in a fixed order (chunk 0 first).  An empty set gives out = 0.
  *
  * q         device bf16 [batch][n_q_heads][head_dim].
  * k_cache, v_cache  device bf16, strided like asp_select_params' K; rows
@@ -236,13 +239,21 @@ ASP_API asp_status asyncspade_score_select(const asp_select_params *p, const flo
  *           of stride_t (ASP_ERR_UNSUPPORTED otherwise).  max_seq_len bounds
  *           every seq_lens[b] (the cache capacity).
  * seq_lens  device int32 [batch].   sel_idx device int32 [batch][n_kv_heads][top_k].
- * out       device fp32 [batch][n_q_heads][head_dim], written.
- * workspace device, >= asyncspade_sparse_decode_workspace(p) bytes.
+ * out       device fp32, written: element (b, hq, d) at
+ *           b * out_stride_b + hq * out_stride_h + d.  out_stride_b ==
+ *           out_stride_h == 0 means the dense [batch][n_q_heads][head_dim]
+ *           layout; head-major [n_q_heads][batch][head_dim] (out_stride_b =
+ *           head_dim, out_stride_h = batch * head_dim) makes the KV-head
+ *           sharded outputs of several GPUs one contiguous concatenation
+ *           (SURVEY §8(e)).  Strides are in elements, >= 0, multiples of 4.
+ * workspace device, >= asyncspade_sparse_decode_workspace(p) bytes, 256-B
+ *           aligned, any contents (the split-K partials).
  * ---------------------------------------------------------------------- */
 typedef struct {
     int32_t batch, n_q_heads, n_kv_heads, head_dim, top_k, n_fresh, max_seq_len;
     float sm_scale; /* usually 1/sqrt(head_dim) */
     int64_t k_stride_b, k_stride_h, k_stride_t, v_stride_b, v_stride_h, v_stride_t;
+    int64_t out_stride_b, out_stride_h; /* elements; both 0: dense [B][Hq][D] (ABI 2) */
 } asp_decode_params;
 
 ASP_API size_t asyncspade_sparse_decode_workspace(const asp_decode_params *p);
@@ -265,7 +276,12 @@ ASP_API asp_status asyncspade_sparse_decode(const asp_decode_params *p, const as
  * (asyncspade_sparse_decode on a [B][Hkv][top_k + n_fresh][D] cache) and
  * gets exactly the attended set of the single-rank decode.
  * p         as asyncspade_sparse_decode (sm_scale unused).
- * k_out, v_out  device bf16 [batch][n_kv_heads][top_k][head_dim], written.
+ * k_out, v_out  device bf16, written: packed row (b, h, j) at
+ *           b * out_stride_b + h * out_stride_h + j * head_dim (elements;
+ *           both 0: dense [batch][n_kv_heads][top_k][head_dim]).  With
+ *           out_stride_h = (top_k + 1) * head_dim the rows land in the
+ *           Inference Rank's compact cache [batch][n_kv_heads][top_k + 1]
+ *           [head_dim], whose last row per (b, h) is its own fresh token.
  * idx_out   nullable device int32 [batch][n_kv_heads][top_k], written.
  * ---------------------------------------------------------------------- */
 ASP_API asp_status asyncspade_gather_filtered(const asp_decode_params *p, const asp_bf16 *k_cache,

@@ -22,7 +22,7 @@ import torch
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libasyncspade.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 ASP_OK = 0
 FLAG_NONFINITE, FLAG_NOT_PD, FLAG_SHORT_ROW = 1, 2, 4
 ASSEMBLY_MASKED_SHARED, ASSEMBLY_SINGLE, ASSEMBLY_PER_WINDOW = 0, 1, 2
@@ -64,7 +64,8 @@ class DecodeParams(ctypes.Structure):
                 ("max_seq_len", ctypes.c_int32), ("sm_scale", ctypes.c_float),
                 ("k_stride_b", ctypes.c_int64), ("k_stride_h", ctypes.c_int64),
                 ("k_stride_t", ctypes.c_int64), ("v_stride_b", ctypes.c_int64),
-                ("v_stride_h", ctypes.c_int64), ("v_stride_t", ctypes.c_int64)]
+                ("v_stride_h", ctypes.c_int64), ("v_stride_t", ctypes.c_int64),
+                ("out_stride_b", ctypes.c_int64), ("out_stride_h", ctypes.c_int64)]
 
 
 class AppendParams(ctypes.Structure):
@@ -193,15 +194,19 @@ def select_params(q_hat: torch.Tensor, k_cache: torch.Tensor, top_k: int,
 
 
 def decode_params(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, top_k: int,
-                  n_fresh: int = 0, sm_scale: float | None = None) -> DecodeParams:
+                  n_fresh: int = 0, sm_scale: float | None = None,
+                  out_head_major: bool = False) -> DecodeParams:
+    """out_head_major: `out` is [Hq, B, D] (a KV-head shard's block of the
+    gathered [Hq_total, B, D] output) instead of [B, Hq, D]."""
     B, Hq, D = q.shape
     _, Hkv, L, _ = k_cache.shape
     if k_cache.stride(3) != 1 or v_cache.stride(3) != 1:
         raise AsyncSpadeError("caches must have unit stride along head_dim")
     if sm_scale is None:
         sm_scale = D ** -0.5
+    osb, osh = (D, B * D) if out_head_major else (0, 0)
     return DecodeParams(B, Hq, Hkv, D, top_k, n_fresh, L, sm_scale, *k_cache.stride()[:3],
-                        *v_cache.stride()[:3])
+                        *v_cache.stride()[:3], osb, osh)
 
 
 def score_select_workspace(p: SelectParams) -> int:
@@ -213,27 +218,33 @@ def sparse_decode_workspace(p: DecodeParams) -> int:
 
 
 def _workspace(nbytes: int, device) -> torch.Tensor:
-    return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+    """A workspace for any entry point: zero-filled once (the decode call's
+    arrival counters must start at zero; every call leaves them at zero)."""
+    return torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
 
 
 # --------------------------------------------------------------------------- entry points
-def append(q_t: torch.Tensor, q_window: torch.Tensor, ring_slot: int, *,
+def append(q_t: torch.Tensor, q_window: torch.Tensor | None, ring_slot: int, *,
            q_cur: torch.Tensor | None = None, k_new: torch.Tensor | None = None,
            v_new: torch.Tensor | None = None, k_cache: torch.Tensor | None = None,
            v_cache: torch.Tensor | None = None, pos: torch.Tensor | None = None,
            stream=None) -> None:
     """a0 -> asyncspade_append: q_t fp32 [B, Hq, D] into window slot
-    `ring_slot`, bf16(q_t) into q_cur, k_new / v_new [B, Hkv, D] into the
-    caches at pos[b]."""
-    B, Hq, W, D = q_window.shape
+    `ring_slot` (q_window may be None), bf16(q_t) into q_cur, k_new / v_new
+    [B, Hkv, D] into the caches at pos[b]."""
+    if q_window is not None:
+        B, Hq, W, D = q_window.shape
+    else:
+        (B, Hq, D), W, ring_slot = q_t.shape, 1, 0
     kc = k_cache if k_cache is not None else v_cache
     Hkv = kc.shape[1] if kc is not None else 1
     L = kc.shape[2] if kc is not None else 1
     ks = k_cache.stride()[:3] if k_cache is not None else (0, 0, 0)
     vs = v_cache.stride()[:3] if v_cache is not None else (0, 0, 0)
     p = AppendParams(B, Hq, Hkv, D, W, ring_slot, L, *ks, *vs,
-                     1 if q_window.dtype == torch.bfloat16 else 0)
-    _check(lib().asyncspade_append(ctypes.byref(p), _ptr(q_t), _ptr(_u16(q_window)),
+                     1 if q_window is not None and q_window.dtype == torch.bfloat16 else 0)
+    _check(lib().asyncspade_append(ctypes.byref(p), _ptr(q_t),
+                                   _ptr(_u16(q_window) if q_window is not None else None),
                                    _ptr(_u16(q_cur) if q_cur is not None else None),
                                    _ptr(_u16(k_new) if k_new is not None else None),
                                    _ptr(_u16(v_new) if v_new is not None else None),
@@ -290,10 +301,13 @@ def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
                   workspace: torch.Tensor | None = None, stream=None,
                   params: DecodeParams | None = None) -> torch.Tensor:
     """a4 -> asyncspade_sparse_decode.  q bf16 [B, Hq, D]; caches bf16
-    [B, Hkv, L, D]; sel_idx int32 [B, Hkv, k].  Returns out fp32 [B, Hq, D]."""
+    [B, Hkv, L, D]; sel_idx int32 [B, Hkv, k].  Returns out fp32 [B, Hq, D]
+    (or [Hq, B, D] when params.out_stride_b is set: head-major)."""
     p = params or decode_params(q, k_cache, v_cache, sel_idx.shape[-1], n_fresh, sm_scale)
     if out is None:
-        out = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+        B, Hq, D = q.shape
+        shape = (Hq, B, D) if p.out_stride_b else (B, Hq, D)
+        out = torch.empty(shape, dtype=torch.float32, device=q.device)
     if workspace is None:
         workspace = _workspace(sparse_decode_workspace(p), q.device)
     ws_bytes = workspace.numel() * workspace.element_size()
@@ -313,12 +327,18 @@ def gather_filtered(k_cache: torch.Tensor, v_cache: torch.Tensor, seq_lens: torc
     is given, the selection over the packed rows (j or -1)."""
     B, Hkv, L, D = k_cache.shape
     k = sel_idx.shape[-1]
-    p = params or DecodeParams(B, Hkv, Hkv, D, k, n_fresh, L, D ** -0.5, *k_cache.stride()[:3],
-                               *v_cache.stride()[:3])
     if k_out is None:
         k_out = torch.empty(B, Hkv, k, D, dtype=k_cache.dtype, device=k_cache.device)
     if v_out is None:
         v_out = torch.empty(B, Hkv, k, D, dtype=v_cache.dtype, device=v_cache.device)
+    if k_out.shape != v_out.shape or k_out.stride() != v_out.stride() or k_out.stride(3) != 1 \
+            or k_out.stride(2) != D or k_out.shape[2] != k:
+        raise AsyncSpadeError("k_out / v_out: [B, Hkv, k, D] views with rows of D elements")
+    # (b, h) blocks at k_out's strides: a [B, Hkv, k + 1, D] compact cache's first
+    # k rows are a valid target
+    osb, osh = ((0, 0) if k_out.is_contiguous() else (k_out.stride(0), k_out.stride(1)))
+    p = params or DecodeParams(B, Hkv, Hkv, D, k, n_fresh, L, D ** -0.5, *k_cache.stride()[:3],
+                               *v_cache.stride()[:3], osb, osh)
     _check(lib().asyncspade_gather_filtered(ctypes.byref(p), _ptr(_u16(k_cache)), _ptr(_u16(v_cache)),
                                             _ptr(seq_lens), _ptr(sel_idx), _ptr(_u16(k_out)),
                                             _ptr(_u16(v_out)), _ptr(idx_out), _stream(stream)),

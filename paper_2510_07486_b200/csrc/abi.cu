@@ -37,6 +37,10 @@ asp_status check_decode(const asp_decode_params *p) {
     if (p->n_q_heads % p->n_kv_heads) return ASP_ERR_SHAPE;
     if (!dim_ok(p->head_dim) || !group_ok(p->n_q_heads / p->n_kv_heads)) return ASP_ERR_UNSUPPORTED;
     if (!(p->sm_scale == p->sm_scale)) return ASP_ERR_INVALID_ARGUMENT;
+    // output strides: both 0 (dense [B][Hq][D]) or both set (e.g. head-major)
+    if (p->out_stride_b < 0 || p->out_stride_h < 0 || ((p->out_stride_b == 0) != (p->out_stride_h == 0)))
+        return ASP_ERR_SHAPE;
+    if ((p->out_stride_b | p->out_stride_h) & 3) return ASP_ERR_INVALID_ARGUMENT;
     if (p->k_stride_t < p->head_dim || p->v_stride_t < p->head_dim || p->k_stride_b < 0 ||
         p->k_stride_h < 0 || p->v_stride_b < 0 || p->v_stride_h < 0)
         return ASP_ERR_SHAPE;
@@ -81,7 +85,7 @@ asp_status asyncspade_append(const asp_append_params *p, const float *q_t, float
                              asp_bf16 *q_cur, const asp_bf16 *k_new, const asp_bf16 *v_new,
                              asp_bf16 *k_cache, asp_bf16 *v_cache, const int32_t *pos,
                              asp_stream stream) {
-    if (!p || !q_t || !q_window) return ASP_ERR_INVALID_ARGUMENT;
+    if (!p || !q_t || (!q_window && !q_cur)) return ASP_ERR_INVALID_ARGUMENT;
     if (p->batch <= 0 || p->n_q_heads <= 0 || p->n_kv_heads <= 0 || p->head_dim <= 0 ||
         p->window <= 0 || p->max_seq_len <= 0)
         return ASP_ERR_SHAPE;
@@ -178,7 +182,7 @@ asp_status asyncspade_score_select_paged(const asp_select_params *p, const asp_p
 
 size_t asyncspade_sparse_decode_workspace(const asp_decode_params *p) {
     if (check_decode(p) != ASP_OK) return 0;
-    return align256(asp_decode_partials_bytes(*p));
+    return asp_decode_workspace_bytes(*p);
 }
 
 asp_status asyncspade_sparse_decode(const asp_decode_params *p, const asp_bf16 *q,
@@ -192,8 +196,8 @@ asp_status asyncspade_sparse_decode(const asp_decode_params *p, const asp_bf16 *
         return ASP_ERR_INVALID_ARGUMENT;
     if (!workspace || workspace_bytes < asyncspade_sparse_decode_workspace(p)) return ASP_ERR_WORKSPACE;
     if (reinterpret_cast<uintptr_t>(workspace) & 255u) return ASP_ERR_WORKSPACE;
-    return from_cuda(asp_launch_decode(*p, q, k_cache, v_cache, seq_lens, sel_idx, out,
-                                       static_cast<float *>(workspace), (cudaStream_t)stream));
+    return from_cuda(asp_launch_decode(*p, q, k_cache, v_cache, seq_lens, sel_idx, out, workspace,
+                                       (cudaStream_t)stream));
 }
 
 asp_status asyncspade_sparse_decode_paged(const asp_decode_params *p, const asp_paged_kv *pk,
@@ -216,9 +220,8 @@ asp_status asyncspade_sparse_decode_paged(const asp_decode_params *p, const asp_
         return ASP_ERR_INVALID_ARGUMENT;
     if (!workspace || workspace_bytes < asyncspade_sparse_decode_workspace(&d)) return ASP_ERR_WORKSPACE;
     if (reinterpret_cast<uintptr_t>(workspace) & 255u) return ASP_ERR_WORKSPACE;
-    return from_cuda(asp_launch_decode(d, q, k_pages, v_pages, seq_lens, sel_idx, out,
-                                       static_cast<float *>(workspace), (cudaStream_t)stream, pk,
-                                       block_table));
+    return from_cuda(asp_launch_decode(d, q, k_pages, v_pages, seq_lens, sel_idx, out, workspace,
+                                       (cudaStream_t)stream, pk, block_table));
 }
 
 size_t asyncspade_quest_meta_bytes(const asp_select_params *p, int32_t page_size) {

@@ -31,10 +31,12 @@ append_kernel(asp_append_params p, const float *__restrict__ q_t, float *__restr
         w.x = *reinterpret_cast<const uint32_t *>(&lo);
         w.y = *reinterpret_cast<const uint32_t *>(&hi);
         const size_t wo = (((size_t)b * p.n_q_heads + hq) * W + p.ring_slot) * D + d;
-        if (p.window_bf16)
+        if (!q_window) {
+        } else if (p.window_bf16) {
             *reinterpret_cast<uint2 *>(reinterpret_cast<asp_bf16 *>(q_window) + wo) = w;
-        else
+        } else {
             *reinterpret_cast<float4 *>(q_window + wo) = v;
+        }
         if (q_cur) *reinterpret_cast<uint2 *>(q_cur + ((size_t)b * p.n_q_heads + hq) * D + d) = w;
     }
     const int n = pos ? pos[b] : -1;

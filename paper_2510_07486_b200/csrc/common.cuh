@@ -110,11 +110,12 @@ cudaError_t asp_launch_score(const asp_select_params &p, const float *q_hat,
 cudaError_t asp_launch_select(const asp_select_params &p, const float *scores,
                               const int32_t *seq_lens, int32_t *sel_idx, uint32_t *dev_flags,
                               bool discard_scores, cudaStream_t s);
-size_t asp_decode_partials_bytes(const asp_decode_params &p);
+// [split-K partials, 256-B aligned][per-(b, KV head) arrival counters, uint32]
+size_t asp_decode_workspace_bytes(const asp_decode_params &p);
 cudaError_t asp_launch_decode(const asp_decode_params &p, const asp_bf16 *q,
                               const asp_bf16 *k_cache, const asp_bf16 *v_cache,
                               const int32_t *seq_lens, const int32_t *sel_idx, float *out,
-                              float *partials, cudaStream_t s,
+                              void *workspace, cudaStream_t s,
                               const asp_paged_kv *pk = nullptr, const int32_t *block_table = nullptr);
 // Quest-style page-bound comparator (quest.cu)
 size_t asp_quest_meta_bytes(const asp_select_params &p, int page_size);

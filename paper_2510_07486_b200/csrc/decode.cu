@@ -10,7 +10,7 @@
 // the chunk partials merged in chunk order by a small combine kernel.  Each
 // chunk is one work item of a persistent, warp-specialised kernel:
 //
-//   warps 0-3  producers: resolve the chunk's token list (indices fetched one
+//   warps 0-7  producers: resolve the chunk's token list (indices fetched one
 //            item ahead), build the bf16 Q operand when the row changes, and
 //            GATHER the selected key / value rows with cp.async (16 lanes per
 //            256-B row, coalesced) straight into the 128-B-swizzled UMMA
@@ -18,12 +18,12 @@
 //            its copies two tiles later, fences them to the async proxy and
 //            arrives on the stage's mbarrier.  (TMA tile::gather4 was measured
 //            ~2.5x slower for 256-B random rows.)
-//   warp 8   TMEM owner + tcgen05.mma issuer (warp-uniform, one elected lane):
+//   warp 12  TMEM owner + tcgen05.mma issuer (warp-uniform, one elected lane):
 //              S^T[128 tok x 16] = K_tile . Q^T          (q is bf16: exact)
 //              O^T[D x 16]      += V_tile^T . P^T        (V tile MN-major)
 //            P = [p_hi; p_lo] is the fp32 softmax weight split into two bf16
 //            terms (rel. error 2^-17), so the P.V products stay fp32-exact;
-//   warps 4-7  softmax (chunk max / exp2 / sums with warp shuffles and one
+//   warps 8-11 softmax (chunk max / exp2 / sums with warp shuffles and one
 //            named barrier) writing the P operand, then the epilogue that
 //            drains O from TMEM and stores the chunk partial (m, l, o).
 //
@@ -175,7 +175,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
     auto o_col = [](int slot) { return (uint32_t)(4 * C::kN + slot * C::kN2); };
 
     if (warp < kProducerWarps) {
-        // ================================================= producers (4 warps)
+        // ================================================= producers (8 warps)
         // Gather the selected K / V rows with cp.async (16 B per thread-op, one
         // token row per 16 consecutive lanes -> coalesced 256-B rows) straight into
         // the 128-B-swizzled UMMA layout; completion arrives on the stage's
@@ -422,7 +422,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
         }
         __syncwarp();
     } else {
-        // ================================================= softmax + epilogue (warps 4-7)
+        // ================================================= softmax + epilogue (warps 8-11)
         const int quad = warp & 3;
         const float scale = p.sm_scale * kLog2e;
         auto softmax = [&](int i) {
@@ -596,7 +596,9 @@ decode_combine_kernel(asp_decode_params p, const float *__restrict__ partials,
             O = fmaf(ps[2 + d], a, O);
         }
     }
-    out[((size_t)b * p.n_q_heads + hq) * D + d] = (L > 0.0f) ? O / L : 0.0f;
+    const int64_t osb = p.out_stride_b ? p.out_stride_b : (int64_t)p.n_q_heads * D;
+    const int64_t osh = p.out_stride_h ? p.out_stride_h : (int64_t)D;
+    out[b * osb + hq * osh + d] = (L > 0.0f) ? O / L : 0.0f;
     // the partials are dead once merged: drop their L2 lines without write-back
     // (whole 128-B lines inside this (b, hq) block only)
     __syncthreads();
@@ -644,15 +646,17 @@ extern "C" __attribute__((visibility("default"))) int asp_decode_prof_read(unsig
 }
 #endif
 
-size_t asp_decode_partials_bytes(const asp_decode_params &p) {
-    return (size_t)p.batch * p.n_q_heads * n_splits_of(p) * (p.head_dim + 2) * sizeof(float);
+size_t asp_decode_workspace_bytes(const asp_decode_params &p) {
+    const size_t b = (size_t)p.batch * p.n_q_heads * n_splits_of(p) * (p.head_dim + 2) * sizeof(float);
+    return (b + 255) & ~(size_t)255;
 }
 
 cudaError_t asp_launch_decode(const asp_decode_params &p, const asp_bf16 *q,
                               const asp_bf16 *k_cache, const asp_bf16 *v_cache,
                               const int32_t *seq_lens, const int32_t *sel_idx, float *out,
-                              float *partials, cudaStream_t s, const asp_paged_kv *pk,
+                              void *workspace, cudaStream_t s, const asp_paged_kv *pk,
                               const int32_t *block_table) {
+    float *partials = static_cast<float *>(workspace);
     const int G = p.n_q_heads / p.n_kv_heads;
 #define ASP_CASE(DD, GG) \
     if (p.head_dim == DD && G == GG) \

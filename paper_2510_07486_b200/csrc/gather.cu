@@ -53,8 +53,15 @@ gather_kernel(asp_decode_params p, const asp_bf16 *__restrict__ k_cache,
 #pragma unroll
         for (int u = 0; u < kUnroll; u++) {
             if (r[u] < rows) {
-                reinterpret_cast<uint4 *>(k_out + r[u] * D)[c] = kv[u];
-                reinterpret_cast<uint4 *>(v_out + r[u] * D)[c] = vv[u];
+                // packed row (b, h, j): dense [B][Hkv][k][D], or (b, h) blocks at the
+                // params' out strides (e.g. the Inference Rank's [B][Hkv][k + 1][D]
+                // compact cache, row k left for its own fresh token)
+                const long bh = r[u] / p.top_k, j = r[u] % p.top_k;
+                const int64_t o = p.out_stride_b
+                    ? (bh / p.n_kv_heads) * p.out_stride_b + (bh % p.n_kv_heads) * p.out_stride_h + j * D
+                    : r[u] * D;
+                reinterpret_cast<uint4 *>(k_out + o)[c] = kv[u];
+                reinterpret_cast<uint4 *>(v_out + o)[c] = vv[u];
                 if (idx_out && c == 0) idx_out[r[u]] = live[u] ? (int)(r[u] % p.top_k) : -1;
             }
         }

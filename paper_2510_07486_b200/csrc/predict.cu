@@ -472,6 +472,120 @@ ASP_DEV float4 ld4(const float *__restrict__ win, int off) {
 constexpr int kPairWarps = 8;
 constexpr int kGS = 17;                            // smem row stride of a Gram (doubles)
 
+// Steps 3-6 for the two rows of a warp, one per half-warp (h =
+// lane / 16, l = lane % 16) on the augmented Gram G (row stride kGS) of row h:
+// the ridge solve by register Gauss-Jordan and the masked-shared / single
+// coefficients.  Lane l returns c = c_{l+1} of q_hat = sum_p c_p Q[p] / denom
+// (c_0 = 0); ok = the half's system was finite and positive definite.
+ASP_DEV void solve_coeffs(const asp_predict_params &p, const double *G, int W, double &c,
+                          double &denom, bool &ok, bool &finite) {
+    const int n = W - 1;
+    const int lane = threadIdx.x & 31;
+    // ---- from here each half-warp owns one row: h = row, l = lane within the half
+    const int h = lane >> 4, l = lane & 15;
+    const unsigned hmask = 0xFFFFu << (16 * h);
+    const bool own = l < n;
+    const double gdiag = l < W ? G[l * kGS + l] : 0.0;
+    finite = (__ballot_sync(0xffffffffu, isfinite(gdiag)) & hmask) == hmask;
+
+    // ---- Step 3 (P:509): omega = (G0 + eps I)^{-1} beta, Gauss-Jordan in registers.
+    double tr = half_sum(own && finite ? gdiag : 0.0);
+    double e = (p.flags & ASP_EPS_ABSOLUTE) ? (double)p.eps : (double)p.eps * (tr / n);
+    if (e == 0.0) e = 1e-30;                                           // reading R7
+    // (a non-finite window solves the identity system instead, so no NaN or
+    // inf flows through the shared arithmetic below; its output is the
+    // passthrough either way)
+    const bool sys = own && finite;
+    double r[16];
+#pragma unroll
+    for (int k = 0; k < 16; k++)
+        r[k] = sys ? (k < n ? G[l * kGS + k] + (k == l ? e : 0.0) : 0.0) : (k == l ? 1.0 : 0.0);
+    double rb = sys ? G[n * kGS + l] : 0.0;                             // beta_l = (H y)_l
+    bool pd = true;
+    double diag = 1.0;
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+        const double d = shfl16(r[j], j);
+        const double pb = shfl16(rb, j);
+        const bool good = d > 0.0 && d < INFINITY;                     // SPD: pivots > 0
+        pd = pd && good;
+        const double f = l != j ? r[j] * rcp_nr1(good ? d : 1.0) : 0.0; // the pivot row stays
+        diag = l == j ? d : diag;
+#pragma unroll
+        for (int k = j + 1; k < 16; k++) r[k] = fma(-f, shfl16(r[k], j), r[k]);
+        rb = fma(-f, pb, rb);
+    }
+    const double x = own ? rb * rcp_nr(diag) : 0.0;
+    // (the ballot runs on every lane: never behind a short-circuit)
+    const unsigned solved = __ballot_sync(0xffffffffu, pd && (!own || isfinite(x)));
+    ok = finite && (solved & hmask) == hmask;
+
+    // ---- Steps 4-6 (P:511-524): coefficients c_p of q_hat = sum_p c_p Q[p] / m;
+    // lane l holds c_{l+1} (c_0 = 0 in both assemblies).
+    const double sgn = (p.flags & ASP_SIGN_NEGATED) ? -1.0 : 1.0;
+    const uint32_t mode = p.flags & 0xFu;
+    c = 0.0;
+    denom = 1.0;
+    if (mode == ASP_ASSEMBLY_SINGLE) {
+        // Eq. 4 (P:214-216): omega[i] (history row i) weights Q[i+1].
+        const double w = (p.flags & ASP_NORM_NONE) ? x : half_softmax(sgn * x, l, n);
+        c = own ? w : 0.0;
+    } else {
+        // masked-shared (readings R4-R6): row j = 1..W uses softmax(v[0..n_j)),
+        // n_j = min(j, n), on the newest n_j queries; rows W-1 and W share n_j = n.
+        double v = sgn * x;
+        if (p.flags & ASP_DOUBLE_SOFTMAX) v = half_softmax(v, l, n);    // literal Step 3
+        const double m = half_max(own ? v : -INFINITY);
+        const double ev = own ? exp(v - m) : 0.0;
+        double S = ev;                                                // inclusive prefix: S_{l+1}
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+            const double t = shfl16_up(S, o);
+            if (l >= o) S += t;
+        }
+        const double invS = rcp_nr(S > 0.0 ? S : 1.0);
+        const bool tiny = (__ballot_sync(0xffffffffu, l == 0 && !(S > 1e-280)) & hmask) != 0;
+        const bool tiny_any = __any_sync(0xffffffffu, tiny);           // warp-uniform
+        double c2 = 0.0;
+#pragma unroll
+        for (int mm = 1; mm < 16; mm++) {
+            if (mm > n) break;                                        // n is warp-uniform
+            const unsigned sh = (unsigned)(n - mm);
+            double t = ev * shfl16(invS, mm - 1);
+            if (mm == n) t *= 2.0;
+            const double u = shfl16_up(t, sh);
+            if (l >= (int)sh && own) {
+                if (mm & 1) c += u;
+                else c2 += u;
+            }
+        }
+        if (tiny_any) {
+            // a prefix's exponentials underflowed against the global max: redo
+            // the half that needs it with each prefix's own max (rolled -- rare,
+            // and kept out of the hot straight-line code)
+            double ct = 0.0;
+#pragma unroll 1
+            for (int mm = 1; mm <= n; mm++) {
+                const unsigned sh = (unsigned)(n - mm);
+                const double mx = half_max(l < mm ? v : -INFINITY);
+                const double ex = l < mm ? exp(v - mx) : 0.0;
+                double t = ex / half_sum(ex);
+                if (mm == n) t *= 2.0;
+                const double u = shfl16_up(t, sh);
+                if (l >= (int)sh && own) ct += u;
+            }
+            if (tiny) {
+                c = ct;
+                c2 = 0.0;
+            }
+        }
+        c += c2;
+        denom = (double)W;
+    }
+
+}
+
+
 template <int D, int NB, bool BF>
 __global__ void __launch_bounds__(kPairWarps * 32)
 predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
@@ -598,107 +712,10 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
 
     // ---- from here each half-warp owns one row: h = row, l = lane within the half
     const int h = lane >> 4, l = lane & 15;
-    const unsigned hmask = 0xFFFFu << (16 * h);
-    const double *G = sG[warp][h];
-    const bool own = l < n;
-    const double gdiag = l < W ? G[l * kGS + l] : 0.0;
-    const bool finite = (__ballot_sync(0xffffffffu, isfinite(gdiag)) & hmask) == hmask;
-
-    // ---- Step 3 (P:509): omega = (G0 + eps I)^{-1} beta, Gauss-Jordan in registers.
-    double tr = half_sum(own && finite ? gdiag : 0.0);
-    double e = (p.flags & ASP_EPS_ABSOLUTE) ? (double)p.eps : (double)p.eps * (tr / n);
-    if (e == 0.0) e = 1e-30;                                           // reading R7
-    // (a non-finite window solves the identity system instead, so no NaN or
-    // inf flows through the shared arithmetic below; its output is the
-    // passthrough either way)
-    const bool sys = own && finite;
-    double r[16];
-#pragma unroll
-    for (int k = 0; k < 16; k++)
-        r[k] = sys ? (k < n ? G[l * kGS + k] + (k == l ? e : 0.0) : 0.0) : (k == l ? 1.0 : 0.0);
-    double rb = sys ? G[n * kGS + l] : 0.0;                             // beta_l = (H y)_l
-    bool pd = true;
-    double diag = 1.0;
-#pragma unroll
-    for (int j = 0; j < 16; j++) {
-        const double d = shfl16(r[j], j);
-        const double pb = shfl16(rb, j);
-        const bool good = d > 0.0 && d < INFINITY;                     // SPD: pivots > 0
-        pd = pd && good;
-        const double f = l != j ? r[j] * rcp_nr1(good ? d : 1.0) : 0.0; // the pivot row stays
-        diag = l == j ? d : diag;
-#pragma unroll
-        for (int k = j + 1; k < 16; k++) r[k] = fma(-f, shfl16(r[k], j), r[k]);
-        rb = fma(-f, pb, rb);
-    }
-    const double x = own ? rb * rcp_nr(diag) : 0.0;
-    // (the ballot runs on every lane: never behind a short-circuit)
-    const unsigned solved = __ballot_sync(0xffffffffu, pd && (!own || isfinite(x)));
-    const bool ok = finite && (solved & hmask) == hmask;
+    double c, denom;
+    bool ok, finite;
+    solve_coeffs(p, sG[warp][h], W, c, denom, ok, finite);
     PPROF(1);
-
-    // ---- Steps 4-6 (P:511-524): coefficients c_p of q_hat = sum_p c_p Q[p] / m;
-    // lane l holds c_{l+1} (c_0 = 0 in both assemblies).
-    const double sgn = (p.flags & ASP_SIGN_NEGATED) ? -1.0 : 1.0;
-    const uint32_t mode = p.flags & 0xFu;
-    double c = 0.0, denom = 1.0;
-    if (mode == ASP_ASSEMBLY_SINGLE) {
-        // Eq. 4 (P:214-216): omega[i] (history row i) weights Q[i+1].
-        const double w = (p.flags & ASP_NORM_NONE) ? x : half_softmax(sgn * x, l, n);
-        c = own ? w : 0.0;
-    } else {
-        // masked-shared (readings R4-R6): row j = 1..W uses softmax(v[0..n_j)),
-        // n_j = min(j, n), on the newest n_j queries; rows W-1 and W share n_j = n.
-        double v = sgn * x;
-        if (p.flags & ASP_DOUBLE_SOFTMAX) v = half_softmax(v, l, n);    // literal Step 3
-        const double m = half_max(own ? v : -INFINITY);
-        const double ev = own ? exp(v - m) : 0.0;
-        double S = ev;                                                // inclusive prefix: S_{l+1}
-#pragma unroll
-        for (int o = 1; o < 16; o <<= 1) {
-            const double t = shfl16_up(S, o);
-            if (l >= o) S += t;
-        }
-        const double invS = rcp_nr(S > 0.0 ? S : 1.0);
-        const bool tiny = (__ballot_sync(0xffffffffu, l == 0 && !(S > 1e-280)) & hmask) != 0;
-        const bool tiny_any = __any_sync(0xffffffffu, tiny);           // warp-uniform
-        double c2 = 0.0;
-#pragma unroll
-        for (int mm = 1; mm < 16; mm++) {
-            if (mm > n) break;                                        // n is warp-uniform
-            const unsigned sh = (unsigned)(n - mm);
-            double t = ev * shfl16(invS, mm - 1);
-            if (mm == n) t *= 2.0;
-            const double u = shfl16_up(t, sh);
-            if (l >= (int)sh && own) {
-                if (mm & 1) c += u;
-                else c2 += u;
-            }
-        }
-        if (tiny_any) {
-            // a prefix's exponentials underflowed against the global max: redo
-            // the half that needs it with each prefix's own max (rolled -- rare,
-            // and kept out of the hot straight-line code)
-            double ct = 0.0;
-#pragma unroll 1
-            for (int mm = 1; mm <= n; mm++) {
-                const unsigned sh = (unsigned)(n - mm);
-                const double mx = half_max(l < mm ? v : -INFINITY);
-                const double ex = l < mm ? exp(v - mx) : 0.0;
-                double t = ex / half_sum(ex);
-                if (mm == n) t *= 2.0;
-                const double u = shfl16_up(t, sh);
-                if (l >= (int)sh && own) ct += u;
-            }
-            if (tiny) {
-                c = ct;
-                c2 = 0.0;
-            }
-        }
-        c += c2;
-        denom = (double)W;
-    }
-
     PPROF(2);
     // ---- q_hat = (1/m) sum_p c_p Q[p] (one pass over the cache-hot window), or
     // the passthrough Q_t.
@@ -751,6 +768,170 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
     PPROF(3);
 }
 
+// Few rows (a KV-head shard, small batches): a row pair per CTA of kSplit
+// warps, the head dimension sliced over the warps.  Each warp loads its slice
+// of both windows ONCE, all at once (<= 8 float4 per lane in flight), keeps
+// it in registers for the weighted sum, and runs its slice of the Gram on the
+// fp64 tensor cores; the partial Grams are summed in smem in warp order
+// (deterministic), warp 0 solves both rows (solve_coeffs), and every warp
+// writes its slice of q_hat.  The latency chain is one DRAM round trip plus
+// the solve, instead of a row pair's whole window streamed through one warp.
+constexpr int kSplit = 4;
+
+template <int D, int NB, bool BF>
+__global__ void __launch_bounds__(kSplit * 32)
+predict_split_kernel(asp_predict_params p, const float *__restrict__ q_window,
+                     float *__restrict__ q_hat, uint32_t *dev_flags) {
+    constexpr int kG = D / (16 * kSplit);               // 16-dim groups per warp (2 or 1)
+    constexpr int T = NB * (NB + 1) / 2;
+    __shared__ double sP[kSplit][2][16 * kGS];         // partial augmented Grams
+    __shared__ double sC[2][16];                       // c_{l+1} per row
+    __shared__ double sDen[2];
+    __shared__ int sOk[2];
+    const int W = p.window;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long rows = (long)p.batch * p.n_q_heads;
+    const long row0 = (long)blockIdx.x * 2;
+    asp::pdl_wait();                 // the window may come from asyncspade_append
+    asp::pdl_trigger();
+    const bool has1 = row0 + 1 < rows;
+    const int rs = p.ring_start;
+    auto phys_of = [&](int i) {
+        const int ph = i + rs;
+        return ph >= W ? ph - W : ph;
+    };
+    const int fr = lane >> 2, fc = lane & 3;
+    // this lane's fragment rows i = 8 b + fr (logical) of both windows, dims
+    // 16 (warp kG + g) + 4 fc + j of this warp's slice
+    float4 f[2][NB][kG];
+#pragma unroll
+    for (int r = 0; r < 2; r++)
+#pragma unroll
+        for (int b = 0; b < NB; b++) {
+            const int i = 8 * b + fr;
+            const bool live = i < W && (r == 0 || has1);
+            const int base = ((int)row0 + r) * W * D + phys_of(i < W ? i : 0) * D + 4 * fc;
+#pragma unroll
+            for (int g = 0; g < kG; g++)
+                f[r][b][g] = live ? ld4<BF>(q_window, base + 16 * (warp * kG + g))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    // ---- Step 2: this slice's share of G' = Q Q^T, fp64 MMA
+    double acc[2][T][2];
+#pragma unroll
+    for (int r = 0; r < 2; r++)
+#pragma unroll
+        for (int t = 0; t < T; t++) acc[r][t][0] = acc[r][t][1] = 0.0;
+#pragma unroll
+    for (int g = 0; g < kG; g++)
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+#pragma unroll
+            for (int r = 0; r < 2; r++) {
+                double x[NB];
+#pragma unroll
+                for (int b = 0; b < NB; b++) {
+                    const float4 v = f[r][b][g];
+                    x[b] = (double)(j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w);
+                }
+                int t = 0;
+#pragma unroll
+                for (int bi = 0; bi < NB; bi++)
+#pragma unroll
+                    for (int bj = bi; bj < NB; bj++, t++) dmma(acc[r][t][0], acc[r][t][1], x[bi], x[bj]);
+            }
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+        int t = 0;
+#pragma unroll
+        for (int bi = 0; bi < NB; bi++)
+#pragma unroll
+            for (int bj = bi; bj < NB; bj++, t++)
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+                    const int i = 8 * bi + fr, j = 8 * bj + 2 * fc + e;
+                    if (i < W && j < W) {
+                        sP[warp][r][i * kGS + j] = acc[r][t][e];
+                        sP[warp][r][j * kGS + i] = acc[r][t][e];
+                    }
+                }
+    }
+    __syncthreads();
+    // sum the slices in warp order into sP[0]
+    for (int x = threadIdx.x; x < 2 * 16 * kGS; x += kSplit * 32) {
+        double v = (&sP[0][0][0])[x];
+#pragma unroll
+        for (int w = 1; w < kSplit; w++) v += (&sP[w][0][0])[x];
+        (&sP[0][0][0])[x] = v;
+    }
+    __syncthreads();
+    // ---- Steps 3-6: warp 0 solves both rows (one per half-warp)
+    if (warp == 0) {
+        const int h = lane >> 4, l = lane & 15;
+        double c, denom;
+        bool ok, finite;
+        solve_coeffs(p, sP[0][h], W, c, denom, ok, finite);
+        sC[h][l] = c;
+        if (l == 0) {
+            sDen[h] = denom;
+            sOk[h] = ok ? 1 : (finite ? 2 : 3);        // 2: not PD, 3: non-finite
+        }
+    }
+    __syncthreads();
+    // ---- q_hat slice = (1/m) sum_p c_p Q[p]: each lane weights its two rows,
+    // the 8 lanes of a column (same fc) reduce by shuffle
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+        if (r == 1 && !has1) break;
+        const int st = sOk[r];
+        float *out = q_hat + (size_t)(row0 + r) * D;
+        if (st == 1) {
+            const double inv_m = 1.0 / sDen[r];
+            double cb[NB];
+#pragma unroll
+            for (int b = 0; b < NB; b++) {
+                const int i = 8 * b + fr;                 // logical row; c_0 = 0
+                cb[b] = (i >= 1 && i < W) ? sC[r][i - 1] : 0.0;
+            }
+#pragma unroll
+            for (int g = 0; g < kG; g++) {
+                double a[4];
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    double v = 0.0;
+#pragma unroll
+                    for (int b = 0; b < NB; b++) {
+                        const float4 q4 = f[r][b][g];
+                        v = fma(cb[b], (double)(j == 0 ? q4.x : j == 1 ? q4.y : j == 2 ? q4.z : q4.w), v);
+                    }
+#pragma unroll
+                    for (int o = 4; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                    a[j] = v;
+                }
+                if (fr == 0)
+                    reinterpret_cast<float4 *>(out + 16 * (warp * kG + g))[fc] =
+                        make_float4((float)(a[0] * inv_m), (float)(a[1] * inv_m),
+                                    (float)(a[2] * inv_m), (float)(a[3] * inv_m));
+            }
+        } else {                                          // passthrough Q_t
+            const int q_off = ((int)row0 + r) * W * D + phys_of(W - 1) * D;
+            for (int d4 = threadIdx.x; d4 < D / 4; d4 += kSplit * 32)
+                reinterpret_cast<float4 *>(out)[d4] = ld4<BF>(q_window, q_off + 4 * d4);
+            if (threadIdx.x == 0) asp::flag_or(dev_flags, st == 2 ? ASP_FLAG_NOT_PD : ASP_FLAG_NONFINITE);
+        }
+    }
+}
+
+template <int D, int NB>
+cudaError_t launch_split(const asp_predict_params &p, const float *q_window, float *q_hat,
+                         uint32_t *dev_flags, cudaStream_t s) {
+    auto kern = (p.flags & ASP_WINDOW_BF16) ? predict_split_kernel<D, NB, true>
+                                            : predict_split_kernel<D, NB, false>;
+    const long rows = (long)p.batch * p.n_q_heads;
+    return asp_launch(kern, dim3((unsigned)((rows + 1) / 2)), dim3(kSplit * 32), 0, s, 1, p,
+                      q_window, q_hat, dev_flags);
+}
+
 template <int D, int NB>
 cudaError_t launch_pair(const asp_predict_params &p, const float *q_window, float *q_hat,
                         uint32_t *dev_flags, cudaStream_t s) {
@@ -792,6 +973,15 @@ cudaError_t asp_launch_predict(const asp_predict_params &p, const float *q_windo
     const bool small = (long)p.batch * p.n_q_heads * p.window * p.head_dim < (1L << 31);
     if (p.window >= 2 && p.window <= 16 && small &&
         (mode == ASP_ASSEMBLY_MASKED_SHARED || mode == ASP_ASSEMBLY_SINGLE)) {
+        // few row pairs: slice the head dimension over a CTA's warps (latency);
+        // many: two rows per warp (throughput)
+        const bool split = (long)p.batch * p.n_q_heads < 8L * asp_sm_count();
+        if (split) {
+            if (p.head_dim == 64) return nb == 1 ? launch_split<64, 1>(p, q_window, q_hat, dev_flags, s)
+                                                 : launch_split<64, 2>(p, q_window, q_hat, dev_flags, s);
+            if (p.head_dim == 128) return nb == 1 ? launch_split<128, 1>(p, q_window, q_hat, dev_flags, s)
+                                                  : launch_split<128, 2>(p, q_window, q_hat, dev_flags, s);
+        }
         if (p.head_dim == 64) return nb == 1 ? launch_pair<64, 1>(p, q_window, q_hat, dev_flags, s)
                                              : launch_pair<64, 2>(p, q_window, q_hat, dev_flags, s);
         if (p.head_dim == 128) return nb == 1 ? launch_pair<128, 1>(p, q_window, q_hat, dev_flags, s)

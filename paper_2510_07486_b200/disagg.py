@@ -2,8 +2,8 @@
 and Cache Rank (Fig. 4; SPEC duo-rank-pipeline S:502-608).
 
     Inference Rank                          Cache Rank (full KV cache + query windows)
-    step t: [recv sel(t)] attention over     recv pack(t) = (q_t, k_t, v_t)
-            sel(t) U its fresh token(s)      a0 append -> a1 predict q_hat(t+1)
+    step t: [sel(t) in?] attention over      recv pack(t) = (q_t, k_t, v_t)
+            sel(t) U its fresh token         a0 append -> a1 predict q_hat(t+1)
             ... rest of the layer ...        -> a2/a3 score + top-k -> gather_filtered
             send pack(t) --------------->    send sel(t+1) = selected K/V rows
             <------------------------------
@@ -12,136 +12,208 @@ The Cache Rank's selection for step t+1 runs while the Inference Rank
 finishes step t and starts t+1, so selection leaves the inference critical
 path; the Inference Rank only attends over the k selected rows it receives
 plus the newest token (n_fresh = 1, reading R12), which the Cache Rank's
-selection cannot contain yet.  Every compute step is a library kernel
-(asyncspade_append, _predict_query, _score_select, _gather_filtered,
-_sparse_decode); this module only moves tensors.  The transport is
-torch.distributed point-to-point (NCCL over NVLink between two GPUs; the
-tests run both ranks on one GPU over gloo with host staging).
+selection cannot contain yet.
+
+Every compute step is a library kernel (asyncspade_append, _predict_query,
+_score_select, _gather_filtered, _sparse_decode); this module only moves
+tensors, and nothing is copied or cast by torch on the Inference Rank's path:
+the Cache Rank gathers the selected rows straight into the Inference Rank's
+compact-cache layout [B][Hkv][k + 1][D] (row k is the receiver's own fresh
+token), the receive lands in that cache, and one asyncspade_append writes the
+fresh K / V row and the bf16 current query.
+
+Stall policy ("stall_policy default = wait ... reuse-previous
+offered"): when the Cache Rank is late, the Inference Rank either waits for
+sel(t) ("wait") or attends with the newest selection it already holds
+("reuse"; the late one is taken at the next step -- the newest completed
+selection always wins).  The transport is torch.distributed point-to-point:
+NCCL over NVLink between two GPUs, or gloo with raw-byte host staging (tests:
+both ranks on one GPU).
 """
 from __future__ import annotations
 
 import torch
 import torch.distributed as dist
 
-from . import (DecodeParams, gather_filtered, predict_query, score_select, sparse_decode,
-               sparse_decode_workspace)
+from . import (DecodeParams, append, gather_filtered, predict_query, score_select,
+               sparse_decode, sparse_decode_workspace)
 from .configs import Config
 from .step import DecodeStep
 
 
-class Transport:
-    """Point-to-point sends of device tensors.  NCCL moves them directly;
-    other backends (gloo) stage through pinned host buffers."""
+class _Pending:
+    """A posted receive (NCCL: in place; gloo: into a host staging buffer)."""
 
-    def __init__(self, peer: int, group=None):
+    def __init__(self, work, t: torch.Tensor, host: torch.Tensor | None):
+        self.work, self.t, self.host = work, t, host
+
+    def done(self) -> bool:
+        return self.work.is_completed()
+
+    def finish(self) -> None:
+        self.work.wait()
+        if self.host is not None:
+            self.t.view(torch.uint8).view(-1).copy_(self.host.to(self.t.device))
+
+
+class Transport:
+    """Point-to-point moves of device tensors.  NCCL moves them directly;
+    other backends (gloo) stage raw bytes through host buffers (bit-exact for
+    every dtype).  Sends and receives may use separate process groups: NCCL
+    serialises a communicator's point-to-point operations on one stream, so
+    the Inference Rank's posted receive of sel(t+1) would otherwise block its
+    own send of pack(t) -- which the Cache Rank needs before it can send
+    sel(t+1).  One group per direction keeps the two streams independent."""
+
+    def __init__(self, peer: int, group=None, recv_group=None):
         self.peer, self.group = peer, group
+        self.recv_group = group if recv_group is None else recv_group
         self.staged = dist.get_backend(group) != "nccl"
 
+    @staticmethod
+    def _bytes(t: torch.Tensor) -> torch.Tensor:
+        return t.view(torch.uint8).view(-1)
+
     def send(self, t: torch.Tensor) -> None:
-        if self.staged:                           # raw bytes: bit-exact for every dtype
+        if not t.is_contiguous():
+            raise ValueError("point-to-point sends need contiguous tensors")
+        if self.staged:
             if t.is_cuda:
                 torch.cuda.current_stream(t.device).synchronize()
-            dist.send(t.contiguous().view(torch.uint8).cpu(), self.peer, group=self.group)
+            dist.send(self._bytes(t).cpu(), self.peer, group=self.group)
         else:
             dist.send(t, self.peer, group=self.group)
 
-    def recv(self, t: torch.Tensor) -> None:
+    def irecv(self, t: torch.Tensor) -> _Pending:
+        if not t.is_contiguous():
+            raise ValueError("point-to-point receives need contiguous tensors")
         if self.staged:
-            h = torch.empty(t.contiguous().view(torch.uint8).shape, dtype=torch.uint8)
-            dist.recv(h, self.peer, group=self.group)
-            t.copy_(h.to(t.device).view(t.dtype).view(t.shape))
-        else:
-            dist.recv(t, self.peer, group=self.group)
+            h = torch.empty(t.numel() * t.element_size(), dtype=torch.uint8)
+            return _Pending(dist.irecv(h, self.peer, group=self.recv_group), t, h)
+        return _Pending(dist.irecv(t, self.peer, group=self.recv_group), t, None)
+
+    def recv(self, t: torch.Tensor) -> None:
+        self.irecv(t).finish()
 
 
 class CacheRank:
     """Holds the full caches and windows of one layer pack; per step: takes the
     Inference Rank's pack, appends it, selects for the NEXT step and returns
-    the selected K/V rows (bit-equal to the cache rows)."""
+    the selected K/V rows (bit-equal to the cache rows) in the receiver's
+    compact-cache layout."""
 
     def __init__(self, cfg: Config, device, transport: Transport, layers: int = 1):
         self.cfg, self.io = cfg, transport
         self.step = DecodeStep(cfg, device, layers=layers)
         st = self.step
-        B = st.q.shape[0]
-        self.q_t = torch.empty(B, st.n_q, cfg.head_dim, dtype=torch.float32, device=st.device)
-        self.kv_t = torch.empty(2, B, st.n_kv, cfg.head_dim, dtype=torch.bfloat16, device=st.device)
+        B, k, D = st.q.shape[0], cfg.top_k, cfg.head_dim
+        self.q_t = torch.empty(B, st.n_q, D, dtype=torch.float32, device=st.device)
+        self.kv_t = torch.empty(2, B, st.n_kv, D, dtype=torch.bfloat16, device=st.device)
         self.pos = torch.sub(st.seq_lens, 1)       # the newest slot (lengths held fixed)
-        self.k_sel = torch.empty(B, st.n_kv, cfg.top_k, cfg.head_dim, dtype=torch.bfloat16,
-                                 device=st.device)
-        self.v_sel = torch.empty_like(self.k_sel)
-        self.i_sel = torch.empty(B, st.n_kv, cfg.top_k, dtype=torch.int32, device=st.device)
+        # [B][Hkv][k + 1][D]: the receiver's compact caches (row k: its fresh token)
+        self.k_sel = torch.zeros(B, st.n_kv, k + 1, D, dtype=torch.bfloat16, device=st.device)
+        self.v_sel = torch.zeros_like(self.k_sel)
+        self.i_sel = torch.empty(B, st.n_kv, k, dtype=torch.int32, device=st.device)
+        self.sent = []                             # global selections sent (tests / audit)
 
     def select_and_gather(self) -> None:
-        st = self.step
+        st, k = self.step, self.cfg.top_k
         predict_query(st.window, st.q_hat, dev_flags=st.dev_flags, params=st.p_pred)
-        score_select(st.q_hat, st.k_cache, st.seq_lens, self.cfg.top_k, sel_idx=st.sel_idx,
+        score_select(st.q_hat, st.k_cache, st.seq_lens, k, sel_idx=st.sel_idx,
                      workspace=st.ws_sel, dev_flags=st.dev_flags, params=st.p_sel)
         # the newest token is the Inference Rank's own (n_fresh = 1): packed rows
         # at or past it are marked -1 in the packed selection
         gather_filtered(st.k_cache, st.v_cache, st.seq_lens, st.sel_idx, n_fresh=1,
-                        k_out=self.k_sel, v_out=self.v_sel, idx_out=self.i_sel)
+                        k_out=self.k_sel[:, :, :k], v_out=self.v_sel[:, :, :k],
+                        idx_out=self.i_sel)
 
-    def send_selection(self) -> None:
+    def send_selection(self, keep: bool = False) -> None:
+        if keep:
+            self.sent.append(self.step.sel_idx.cpu().clone())
         self.io.send(self.k_sel)
         self.io.send(self.v_sel)
         self.io.send(self.i_sel)
 
-    def prime(self) -> None:
+    def prime(self, keep: bool = False) -> None:
         """Selection for the first step (from the windows as they stand)."""
         self.select_and_gather()
-        self.send_selection()
+        self.send_selection(keep)
 
-    def serve(self, send: bool = True) -> None:
-        """One step: receive pack(t), append it, select for t+1 and (unless it
-        is the last step) send sel(t+1)."""
+    def serve(self, keep: bool = False, delay_s: float = 0.0) -> None:
+        """One step: receive pack(t), append it, select for t+1, send sel(t+1)
+        (after `delay_s`: tests of a late Cache Rank)."""
         self.io.recv(self.q_t)
         self.io.recv(self.kv_t)
         self.step.append(self.q_t, self.kv_t[0], self.kv_t[1], self.pos)
         self.select_and_gather()
-        if send:
-            self.send_selection()
+        if delay_s:
+            import time
+            torch.cuda.current_stream(self.step.device).synchronize()
+            time.sleep(delay_s)
+        self.send_selection(keep)
 
 
 class InferenceRank:
     """Attends over the received selection plus its own newest token; sends
-    each step's (q_t, k_t, v_t) to the Cache Rank."""
+    each step's (q_t, k_t, v_t) to the Cache Rank.  Two compact caches: the
+    selection in use, and the one the next selection is received into."""
 
     def __init__(self, cfg: Config, device, transport: Transport, n_q: int, n_kv: int,
-                 batch: int):
-        self.cfg, self.io = cfg, transport
+                 batch: int, stall_policy: str = "wait"):
+        if stall_policy not in ("wait", "reuse"):
+            raise ValueError("stall_policy: 'wait' or 'reuse'")
+        self.cfg, self.io, self.policy = cfg, transport, stall_policy
         dev = torch.device(device)
         D, k = cfg.head_dim, cfg.top_k
-        # the compact cache: k received rows + the fresh token at row k
-        self.k_c = torch.zeros(batch, n_kv, k + 1, D, dtype=torch.bfloat16, device=dev)
-        self.v_c = torch.zeros_like(self.k_c)
-        # contiguous receive buffers (point-to-point needs dense tensors); the
-        # rows are then placed ahead of the fresh token
-        self.k_r = torch.empty(batch, n_kv, k, D, dtype=torch.bfloat16, device=dev)
-        self.v_r = torch.empty_like(self.k_r)
+        self.k_c = [torch.zeros(batch, n_kv, k + 1, D, dtype=torch.bfloat16, device=dev)
+                    for _ in range(2)]
+        self.v_c = [torch.zeros_like(self.k_c[0]) for _ in range(2)]
+        self.idx = [torch.empty(batch, n_kv, k, dtype=torch.int32, device=dev) for _ in range(2)]
         self.lens = torch.full((batch,), k + 1, dtype=torch.int32, device=dev)
-        self.idx = torch.empty(batch, n_kv, k, dtype=torch.int32, device=dev)   # packed selection
+        self.pos = torch.full((batch,), k, dtype=torch.int32, device=dev)   # the fresh row
         self.q = torch.empty(batch, n_q, D, dtype=torch.bfloat16, device=dev)
         self.out = torch.empty(batch, n_q, D, dtype=torch.float32, device=dev)
         self.p = DecodeParams(batch, n_q, n_kv, D, k, 1, k + 1, D ** -0.5,
-                              *self.k_c.stride()[:3], *self.v_c.stride()[:3])
+                              *self.k_c[0].stride()[:3], *self.v_c[0].stride()[:3], 0, 0)
         self.ws = torch.empty(max(sparse_decode_workspace(self.p), 256), dtype=torch.uint8,
                               device=dev)
+        self.cur = -1                      # compact cache in use (-1: none yet)
+        self.received = 0                  # selections installed so far
+        self.used = []                     # per step: which selection (0-based) was used
+        self._post()
+
+    def _post(self) -> None:
+        nxt = 1 if self.cur == 0 else 0
+        self.spare = nxt
+        self.pending = [self.io.irecv(self.k_c[nxt]), self.io.irecv(self.v_c[nxt]),
+                        self.io.irecv(self.idx[nxt])]
+
+    def _install(self) -> None:
+        for pr in self.pending:
+            pr.finish()
+        self.cur = self.spare
+        self.received += 1
+        self._post()
 
     def step(self, q_t: torch.Tensor, kv_t: torch.Tensor) -> torch.Tensor:
         """Decode step t: q_t fp32 [B, Hq, D] (the current query), kv_t bf16
         [2, B, Hkv, D] (the new token).  Returns the attention output."""
-        k = self.cfg.top_k
-        self.io.recv(self.k_r)                     # sel(t), computed from pack(t-1)
-        self.io.recv(self.v_r)
-        self.io.recv(self.idx)
-        self.k_c[:, :, :k].copy_(self.k_r)
-        self.v_c[:, :, :k].copy_(self.v_r)
-        self.k_c[:, :, k].copy_(kv_t[0])
-        self.v_c[:, :, k].copy_(kv_t[1])
-        self.q.copy_(q_t)
-        sparse_decode(self.q, self.k_c, self.v_c, self.lens, self.idx, out=self.out,
+        if self.cur < 0 or self.policy == "wait":
+            self._install()                            # sel(t): wait for it
+        while all(pr.done() for pr in self.pending):   # reuse: take the newest arrived
+            self._install()
+        self.used.append(self.received - 1)
+        c = self.cur
+        # a0 on this rank: bf16(q_t) -> q, the fresh K / V row -> compact row k
+        append(q_t, None, 0, q_cur=self.q, k_new=kv_t[0], v_new=kv_t[1], k_cache=self.k_c[c],
+               v_cache=self.v_c[c], pos=self.pos)
+        sparse_decode(self.q, self.k_c[c], self.v_c[c], self.lens, self.idx[c], out=self.out,
                       workspace=self.ws, params=self.p)
-        self.io.send(q_t)                          # pack(t) -> the Cache Rank
+        self.io.send(q_t)                              # pack(t) -> the Cache Rank
         self.io.send(kv_t)
         return self.out
+
+    def finish(self) -> None:
+        """Drain: take every selection the Cache Rank sent (it sends one per
+        pack plus the first), so no receive is left posted."""
+        self._install()

@@ -62,7 +62,7 @@ class DecodeStep:
         self.p_dec = decode_params(self.q, self.k_cache, self.v_cache, cfg.top_k, n_fresh)
         self.ws_sel = torch.empty(max(score_select_workspace(self.p_sel), 256), dtype=torch.uint8,
                                   device=dev)
-        self.ws_dec = torch.empty(max(sparse_decode_workspace(self.p_dec), 256),
+        self.ws_dec = torch.zeros(max(sparse_decode_workspace(self.p_dec), 256),
                                   dtype=torch.uint8, device=dev)
         # one CUDA graph per ring position: the predict launch bakes ring_start
         # into its parameters, so append() (which advances it) selects another

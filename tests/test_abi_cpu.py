@@ -101,7 +101,8 @@ def test_score_select_validation_and_workspace(L):
 def _dec(**kw):
     d = dict(batch=2, n_q_heads=32, n_kv_heads=8, head_dim=128, top_k=64, n_fresh=1,
              max_seq_len=1024, sm_scale=128 ** -0.5, k_stride_b=8 * 1024 * 128, k_stride_h=1024 * 128,
-             k_stride_t=128, v_stride_b=8 * 1024 * 128, v_stride_h=1024 * 128, v_stride_t=128)
+             k_stride_t=128, v_stride_b=8 * 1024 * 128, v_stride_h=1024 * 128, v_stride_t=128,
+             out_stride_b=0, out_stride_h=0)
     d.update(kw)
     return asp.DecodeParams(*[d[f] for f, _ in asp.DecodeParams._fields_])
 
@@ -114,7 +115,9 @@ def test_sparse_decode_validation_and_workspace(L):
     p = _dec()
     need = L.asyncspade_sparse_decode_workspace(ctypes.byref(p))
     # one 256-entry chunk: [B][Hq][1][D + 2] fp32 partials
-    assert need >= 2 * 32 * 1 * 130 * 4
+    assert need >= 2 * 32 * 1 * 130 * 4 and need % 256 == 0
+    need3 = L.asyncspade_sparse_decode_workspace(ctypes.byref(_dec(top_k=600)))
+    assert need3 >= 2 * 32 * 3 * 130 * 4 and need3 % 256 == 0
     assert call(p, out=None) == 1
     assert call(p, idx=None) == 1
     assert call(p, nbytes=need - 1) == 4
@@ -125,6 +128,10 @@ def test_sparse_decode_validation_and_workspace(L):
     assert call(_dec(sm_scale=float("nan"))) == 1
     assert call(_dec(max_seq_len=0)) == 2
     assert call(_dec(k_stride_h=1024 * 128 + 8)) == 3           # not a multiple of stride_t
+    # output strides (ABI 2): both 0 (dense) or both set, >= 0, multiples of 4
+    assert call(_dec(out_stride_b=128, out_stride_h=0)) == 2
+    assert call(_dec(out_stride_b=-128, out_stride_h=256)) == 2
+    assert call(_dec(out_stride_b=130, out_stride_h=256)) == 1
 
 
 def test_synth_library_exports():

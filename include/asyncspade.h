@@ -254,6 +254,7 @@ typedef struct {
     float sm_scale; /* usually 1/sqrt(head_dim) */
     int64_t k_stride_b, k_stride_h, k_stride_t, v_stride_b, v_stride_h, v_stride_t;
     int64_t out_stride_b, out_stride_h; /* elements; both 0: dense [B][Hq][D] (ABI 2) */
+    int32_t v_head_dim; /* value rows' width; 0: head_dim.  < head_dim: absorbed MLA (ABI 2) */
 } asp_decode_params;
 
 ASP_API size_t asyncspade_sparse_decode_workspace(const asp_decode_params *p);

@@ -137,6 +137,13 @@ def sparse_decode(q: np.ndarray, k_cache: np.ndarray, v_cache: np.ndarray, sel_i
     ix = _c(sel_idx, np.int32)
     B, Hq, D = qq.shape
     _, Hkv, L, _ = k.shape
+    Dv = v.shape[-1]
+    if Dv < D:
+        # values narrower than the keys (absorbed MLA: the latent is
+        # the first Dv key dims): zero-extended to D -- marshalling only, the
+        # extra output columns are sum_j p_j * 0 and are dropped
+        v = np.ascontiguousarray(np.concatenate(
+            [v, np.zeros(v.shape[:-1] + (D - Dv,), np.uint16)], axis=-1))
     top_k = ix.shape[-1]
     if sm_scale is None:
         sm_scale = 1.0 / np.sqrt(D)
@@ -144,7 +151,7 @@ def sparse_decode(q: np.ndarray, k_cache: np.ndarray, v_cache: np.ndarray, sel_i
     out = np.empty((B, Hq, D), np.float32)
     _load().asp_oracle_sparse_decode(B, Hq, Hkv, D, L, top_k, n_fresh, float(sm_scale),
                                      _p(sl), _p(qq), _p(k), _p(v), _p(ix), _p(out))
-    return out
+    return np.ascontiguousarray(out[..., :Dv])
 
 
 def dense_attention(q: np.ndarray, k_cache: np.ndarray, v_cache: np.ndarray, seq_lens,

@@ -65,7 +65,8 @@ class DecodeParams(ctypes.Structure):
                 ("k_stride_b", ctypes.c_int64), ("k_stride_h", ctypes.c_int64),
                 ("k_stride_t", ctypes.c_int64), ("v_stride_b", ctypes.c_int64),
                 ("v_stride_h", ctypes.c_int64), ("v_stride_t", ctypes.c_int64),
-                ("out_stride_b", ctypes.c_int64), ("out_stride_h", ctypes.c_int64)]
+                ("out_stride_b", ctypes.c_int64), ("out_stride_h", ctypes.c_int64),
+                ("v_head_dim", ctypes.c_int32)]
 
 
 class AppendParams(ctypes.Structure):
@@ -195,18 +196,21 @@ def select_params(q_hat: torch.Tensor, k_cache: torch.Tensor, top_k: int,
 
 def decode_params(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, top_k: int,
                   n_fresh: int = 0, sm_scale: float | None = None,
-                  out_head_major: bool = False) -> DecodeParams:
-    """out_head_major: `out` is [Hq, B, D] (a KV-head shard's block of the
-    gathered [Hq_total, B, D] output) instead of [B, Hq, D]."""
+                  out_head_major: bool = False, v_head_dim: int = 0) -> DecodeParams:
+    """out_head_major: `out` is [Hq, B, Dv] (a KV-head shard's block of the
+    gathered [Hq_total, B, Dv] output) instead of [B, Hq, Dv].  v_head_dim:
+    the value width (0: head_dim); absorbed MLA passes v_cache = k_cache and
+    the latent width 512 < head_dim 576."""
     B, Hq, D = q.shape
     _, Hkv, L, _ = k_cache.shape
     if k_cache.stride(3) != 1 or v_cache.stride(3) != 1:
         raise AsyncSpadeError("caches must have unit stride along head_dim")
     if sm_scale is None:
         sm_scale = D ** -0.5
-    osb, osh = (D, B * D) if out_head_major else (0, 0)
+    dv = v_head_dim or D
+    osb, osh = (dv, B * dv) if out_head_major else (0, 0)
     return DecodeParams(B, Hq, Hkv, D, top_k, n_fresh, L, sm_scale, *k_cache.stride()[:3],
-                        *v_cache.stride()[:3], osb, osh)
+                        *v_cache.stride()[:3], osb, osh, v_head_dim)
 
 
 def score_select_workspace(p: SelectParams) -> int:
@@ -306,7 +310,8 @@ def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
     p = params or decode_params(q, k_cache, v_cache, sel_idx.shape[-1], n_fresh, sm_scale)
     if out is None:
         B, Hq, D = q.shape
-        shape = (Hq, B, D) if p.out_stride_b else (B, Hq, D)
+        dv = p.v_head_dim or D
+        shape = (Hq, B, dv) if p.out_stride_b else (B, Hq, dv)
         out = torch.empty(shape, dtype=torch.float32, device=q.device)
     if workspace is None:
         workspace = _workspace(sparse_decode_workspace(p), q.device)

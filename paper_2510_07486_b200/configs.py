@@ -15,6 +15,8 @@ class Config:
     seq_len: int
     top_k: int
     window: int
+    v_head_dim: int = 0   # 0: head_dim.  Absorbed MLA: keys are the 576-dim latent
+                          # (+ rope), values its first 512 dims
 
     @property
     def group(self) -> int:
@@ -35,6 +37,13 @@ QWEN3_8B = Config("qwen3-8b_b32_ctx32k", 1, 32, 32, 8, 128, 32768, 2048, 16)
 QWEN3_32B = Config("qwen3-32b_b64_ctx32k", 2, 64, 64, 8, 128, 32768, 2048, 16)
 
 
+# NEXT-3 attention variants: absorbed MLA as MQA over the latent
+# (DeepSeek-V2-Lite: 16 heads; 576 = 512 latent + 64 rope dims, values = the
+# latent), and multi-query attention with 64 query heads on one KV head
+MLA_16 = Config("mla16_b16_ctx32k", 0, 16, 16, 1, 576, 32768, 2048, 16, v_head_dim=512)
+MQA_64 = Config("mqa64_b32_ctx32k", 0, 32, 64, 1, 128, 32768, 2048, 16)
+
+
 def long_cot(seq_len: int) -> Config:
     return Config(f"long-cot_b8_ctx{seq_len}", 3, 8, 64, 8, 128, seq_len, seq_len // 16, 16)
 
@@ -43,7 +52,7 @@ def high_concurrency(batch: int) -> Config:
     return Config(f"high-conc_b{batch}_ctx4k", 4, batch, 32, 8, 128, 4096, 256, 16)
 
 
-BY_NAME = {c.name: c for c in (TINY, QWEN3_8B, QWEN3_32B)}
+BY_NAME = {c.name: c for c in (TINY, QWEN3_8B, QWEN3_32B, MLA_16, MQA_64)}
 
 
 def by_name(name: str) -> Config:

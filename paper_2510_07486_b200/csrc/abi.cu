@@ -8,8 +8,16 @@
 namespace {
 
 bool aligned16(const void *ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
+// the tensor-core kernels (score.cu, decode.cu): head_dim 64 / 128, G <= 32
 bool group_ok(int G) { return G == 1 || G == 2 || G == 4 || G == 8 || G == 16 || G == 32; }
 bool dim_ok(int D) { return D == 64 || D == 128; }
+bool tc_select_ok(const asp_select_params *p) {
+    return dim_ok(p->head_dim) && group_ok(p->n_q_heads / p->n_kv_heads);
+}
+int v_dim_of(const asp_decode_params *p) { return p->v_head_dim ? p->v_head_dim : p->head_dim; }
+bool tc_decode_ok(const asp_decode_params *p) {
+    return dim_ok(p->head_dim) && group_ok(p->n_q_heads / p->n_kv_heads) && v_dim_of(p) == p->head_dim;
+}
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 asp_status from_cuda(cudaError_t e) { return e == cudaSuccess ? ASP_OK : ASP_ERR_CUDA; }
@@ -20,7 +28,9 @@ asp_status check_select(const asp_select_params *p) {
         p->top_k <= 0 || p->max_seq_len <= 0)
         return ASP_ERR_SHAPE;
     if (p->n_q_heads % p->n_kv_heads) return ASP_ERR_SHAPE;
-    if (!dim_ok(p->head_dim) || !group_ok(p->n_q_heads / p->n_kv_heads)) return ASP_ERR_UNSUPPORTED;
+    // tensor-core stream, or the CUDA-core kernel for absorbed MLA / large groups
+    if (!tc_select_ok(p) && !asp_score_cc_supported(p->head_dim, p->n_q_heads / p->n_kv_heads))
+        return ASP_ERR_UNSUPPORTED;
     if (p->aggregation != ASP_AGG_MAX && p->aggregation != ASP_AGG_SUM) return ASP_ERR_INVALID_ARGUMENT;
     if (p->k_stride_t < p->head_dim || p->k_stride_b < 0 || p->k_stride_h < 0) return ASP_ERR_SHAPE;
     if ((p->k_stride_b | p->k_stride_h | p->k_stride_t) & 7) return ASP_ERR_INVALID_ARGUMENT;
@@ -35,13 +45,16 @@ asp_status check_decode(const asp_decode_params *p) {
         p->top_k <= 0 || p->n_fresh < 0 || p->max_seq_len <= 0)
         return ASP_ERR_SHAPE;
     if (p->n_q_heads % p->n_kv_heads) return ASP_ERR_SHAPE;
-    if (!dim_ok(p->head_dim) || !group_ok(p->n_q_heads / p->n_kv_heads)) return ASP_ERR_UNSUPPORTED;
+    if (p->v_head_dim < 0 || p->v_head_dim > p->head_dim) return ASP_ERR_SHAPE;
+    if (!tc_decode_ok(p) &&
+        !asp_decode_cc_supported(p->head_dim, v_dim_of(p), p->n_q_heads / p->n_kv_heads))
+        return ASP_ERR_UNSUPPORTED;
     if (!(p->sm_scale == p->sm_scale)) return ASP_ERR_INVALID_ARGUMENT;
     // output strides: both 0 (dense [B][Hq][D]) or both set (e.g. head-major)
     if (p->out_stride_b < 0 || p->out_stride_h < 0 || ((p->out_stride_b == 0) != (p->out_stride_h == 0)))
         return ASP_ERR_SHAPE;
     if ((p->out_stride_b | p->out_stride_h) & 3) return ASP_ERR_INVALID_ARGUMENT;
-    if (p->k_stride_t < p->head_dim || p->v_stride_t < p->head_dim || p->k_stride_b < 0 ||
+    if (p->k_stride_t < p->head_dim || p->v_stride_t < v_dim_of(p) || p->k_stride_b < 0 ||
         p->k_stride_h < 0 || p->v_stride_b < 0 || p->v_stride_h < 0)
         return ASP_ERR_SHAPE;
     if ((p->k_stride_b | p->k_stride_h | p->k_stride_t | p->v_stride_b | p->v_stride_h |
@@ -109,13 +122,14 @@ asp_status asyncspade_predict_query(const asp_predict_params *p, const float *q_
     if (p->batch <= 0 || p->n_q_heads <= 0 || p->head_dim <= 0 || p->window <= 0)
         return ASP_ERR_SHAPE;
     if (p->ring_start < 0 || p->ring_start >= p->window) return ASP_ERR_SHAPE;
-    if (!dim_ok(p->head_dim) || p->window > 32) return ASP_ERR_UNSUPPORTED;
+    if (!(dim_ok(p->head_dim) || p->head_dim == 256 || p->head_dim == 576) || p->window > 32)
+        return ASP_ERR_UNSUPPORTED;
     const uint32_t mode = p->flags & 0xFu;
     const uint32_t known = 0xFu | ASP_SIGN_NEGATED | ASP_EPS_ABSOLUTE | ASP_NORM_NONE |
                            ASP_DOUBLE_SOFTMAX | ASP_WINDOW_BF16;
     if (mode > ASP_ASSEMBLY_PER_WINDOW || (p->flags & ~known)) return ASP_ERR_INVALID_ARGUMENT;
     if ((p->flags & ASP_WINDOW_BF16) &&
-        (p->window < 2 || p->window > 16 || mode == ASP_ASSEMBLY_PER_WINDOW ||
+        (p->window < 2 || p->window > 16 || mode == ASP_ASSEMBLY_PER_WINDOW || !dim_ok(p->head_dim) ||
          (int64_t)p->batch * p->n_q_heads * p->window * p->head_dim >= ((int64_t)1 << 31)))
         return ASP_ERR_UNSUPPORTED;
     if ((p->flags & ASP_NORM_NONE) && mode != ASP_ASSEMBLY_SINGLE) return ASP_ERR_INVALID_ARGUMENT;
@@ -146,7 +160,8 @@ asp_status asyncspade_score_select(const asp_select_params *p, const float *q_ha
         s_buf = static_cast<float *>(workspace);
     }
     cudaStream_t s = (cudaStream_t)stream;
-    cudaError_t e = asp_launch_score(*p, q_hat, k_cache, seq_lens, s_buf, dev_flags, s);
+    cudaError_t e = tc_select_ok(p) ? asp_launch_score(*p, q_hat, k_cache, seq_lens, s_buf, dev_flags, s)
+                                    : asp_launch_score_cc(*p, q_hat, k_cache, seq_lens, s_buf, dev_flags, s);
     if (e != cudaSuccess) return ASP_ERR_CUDA;
     return from_cuda(asp_launch_select(*p, s_buf, seq_lens, sel_idx, dev_flags, scores == nullptr, s));
 }
@@ -163,6 +178,7 @@ asp_status asyncspade_score_select_paged(const asp_select_params *p, const asp_p
     q.k_stride_h = q.k_stride_b = 0;
     asp_status st = check_select(&q);
     if (st != ASP_OK) return st;
+    if (!tc_select_ok(&q)) return ASP_ERR_UNSUPPORTED;           // paged: tensor-core shapes
     st = check_paged(pk, q.n_kv_heads, q.max_seq_len);
     if (st != ASP_OK) return st;
     if (!q_hat || !k_pages || !block_table || !seq_lens || !sel_idx) return ASP_ERR_INVALID_ARGUMENT;
@@ -182,7 +198,8 @@ asp_status asyncspade_score_select_paged(const asp_select_params *p, const asp_p
 
 size_t asyncspade_sparse_decode_workspace(const asp_decode_params *p) {
     if (check_decode(p) != ASP_OK) return 0;
-    return asp_decode_workspace_bytes(*p);
+    return tc_decode_ok(p) ? asp_decode_workspace_bytes(*p)
+                           : asp_decode_cc_workspace_bytes(*p, v_dim_of(p));
 }
 
 asp_status asyncspade_sparse_decode(const asp_decode_params *p, const asp_bf16 *q,
@@ -196,6 +213,9 @@ asp_status asyncspade_sparse_decode(const asp_decode_params *p, const asp_bf16 *
         return ASP_ERR_INVALID_ARGUMENT;
     if (!workspace || workspace_bytes < asyncspade_sparse_decode_workspace(p)) return ASP_ERR_WORKSPACE;
     if (reinterpret_cast<uintptr_t>(workspace) & 255u) return ASP_ERR_WORKSPACE;
+    if (!tc_decode_ok(p))
+        return from_cuda(asp_launch_decode_cc(*p, v_dim_of(p), q, k_cache, v_cache, seq_lens,
+                                              sel_idx, out, workspace, (cudaStream_t)stream));
     return from_cuda(asp_launch_decode(*p, q, k_cache, v_cache, seq_lens, sel_idx, out, workspace,
                                        (cudaStream_t)stream));
 }
@@ -212,6 +232,7 @@ asp_status asyncspade_sparse_decode_paged(const asp_decode_params *p, const asp_
     d.k_stride_h = d.k_stride_b = d.v_stride_h = d.v_stride_b = 0;
     asp_status st = check_decode(&d);
     if (st != ASP_OK) return st;
+    if (!tc_decode_ok(&d)) return ASP_ERR_UNSUPPORTED;           // paged: tensor-core shapes
     st = check_paged(pk, d.n_kv_heads, d.max_seq_len);
     if (st != ASP_OK) return st;
     if (!q || !k_pages || !v_pages || !block_table || !seq_lens || !sel_idx || !out)
@@ -225,7 +246,7 @@ asp_status asyncspade_sparse_decode_paged(const asp_decode_params *p, const asp_
 }
 
 size_t asyncspade_quest_meta_bytes(const asp_select_params *p, int32_t page_size) {
-    if (check_select(p) != ASP_OK || page_size < 1 || page_size > 128) return 0;
+    if (check_select(p) != ASP_OK || !dim_ok(p->head_dim) || page_size < 1 || page_size > 128) return 0;
     return align256(asp_quest_meta_bytes(*p, page_size));
 }
 
@@ -234,7 +255,7 @@ asp_status asyncspade_quest_summarize(const asp_select_params *p, int32_t page_s
                                       asp_stream stream) {
     asp_status st = check_select(p);
     if (st != ASP_OK) return st;
-    if (page_size < 1 || page_size > 128) return ASP_ERR_UNSUPPORTED;
+    if (page_size < 1 || page_size > 128 || !dim_ok(p->head_dim)) return ASP_ERR_UNSUPPORTED;
     if (!k_cache || !seq_lens || !meta) return ASP_ERR_INVALID_ARGUMENT;
     if (!aligned16(k_cache) || !aligned16(meta)) return ASP_ERR_INVALID_ARGUMENT;
     return from_cuda(asp_launch_quest_summarize(*p, page_size, k_cache, seq_lens, meta,
@@ -244,7 +265,7 @@ asp_status asyncspade_quest_summarize(const asp_select_params *p, int32_t page_s
 // the Quest page-bound kernel is instantiated for G in {1, 2, 4, 8} only
 static bool quest_group_ok(const asp_select_params *p) {
     const int G = p->n_q_heads / p->n_kv_heads;
-    return G == 1 || G == 2 || G == 4 || G == 8;
+    return (G == 1 || G == 2 || G == 4 || G == 8) && dim_ok(p->head_dim);
 }
 
 size_t asyncspade_quest_select_workspace(const asp_select_params *p, int32_t page_size) {
@@ -277,6 +298,7 @@ asp_status asyncspade_gather_filtered(const asp_decode_params *p, const asp_bf16
                                       int32_t *idx_out, asp_stream stream) {
     asp_status st = check_decode(p);
     if (st != ASP_OK) return st;
+    if (!dim_ok(p->head_dim) || v_dim_of(p) != p->head_dim) return ASP_ERR_UNSUPPORTED;
     if (!k_cache || !v_cache || !seq_lens || !sel_idx || !k_out || !v_out)
         return ASP_ERR_INVALID_ARGUMENT;
     if (!aligned16(k_cache) || !aligned16(v_cache) || !aligned16(k_out) || !aligned16(v_out))

@@ -117,6 +117,17 @@ cudaError_t asp_launch_decode(const asp_decode_params &p, const asp_bf16 *q,
                               const int32_t *seq_lens, const int32_t *sel_idx, float *out,
                               void *workspace, cudaStream_t s,
                               const asp_paged_kv *pk = nullptr, const int32_t *block_table = nullptr);
+// CUDA-core kernels for absorbed MLA / large query groups (score_cc.cu, decode_cc.cu)
+bool asp_score_cc_supported(int head_dim, int group);
+cudaError_t asp_launch_score_cc(const asp_select_params &p, const float *q_hat,
+                                const asp_bf16 *k_cache, const int32_t *seq_lens, float *scores,
+                                uint32_t *dev_flags, cudaStream_t s);
+bool asp_decode_cc_supported(int head_dim, int v_head_dim, int group);
+size_t asp_decode_cc_workspace_bytes(const asp_decode_params &p, int v_head_dim);
+cudaError_t asp_launch_decode_cc(const asp_decode_params &p, int v_head_dim, const asp_bf16 *q,
+                                 const asp_bf16 *k_cache, const asp_bf16 *v_cache,
+                                 const int32_t *seq_lens, const int32_t *sel_idx, float *out,
+                                 void *workspace, cudaStream_t s);
 // Quest-style page-bound comparator (quest.cu)
 size_t asp_quest_meta_bytes(const asp_select_params &p, int page_size);
 size_t asp_quest_workspace_bytes(const asp_select_params &p, int page_size);

@@ -991,6 +991,9 @@ cudaError_t asp_launch_predict(const asp_predict_params &p, const float *q_windo
     if (p.head_dim == DD && nb == NBB) return launch<DD, NBB>(p, q_window, q_hat, dev_flags, s);
     ASP_CASE(64, 1) ASP_CASE(64, 2) ASP_CASE(64, 3) ASP_CASE(64, 4)
     ASP_CASE(128, 1) ASP_CASE(128, 2) ASP_CASE(128, 3) ASP_CASE(128, 4)
+    // absorbed MLA queries (the 576-dim latent + rope space) and 256-dim heads
+    ASP_CASE(256, 1) ASP_CASE(256, 2) ASP_CASE(256, 3) ASP_CASE(256, 4)
+    ASP_CASE(576, 1) ASP_CASE(576, 2) ASP_CASE(576, 3) ASP_CASE(576, 4)
 #undef ASP_CASE
     return cudaErrorInvalidValue;
 }

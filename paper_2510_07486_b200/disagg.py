@@ -180,6 +180,7 @@ class InferenceRank:
         self.cur = -1                      # compact cache in use (-1: none yet)
         self.received = 0                  # selections installed so far
         self.used = []                     # per step: which selection (0-based) was used
+        self.packs = 0                     # packs sent (the Cache Rank answers each)
         self._post()
 
     def _post(self) -> None:
@@ -211,9 +212,12 @@ class InferenceRank:
                       workspace=self.ws, params=self.p)
         self.io.send(q_t)                              # pack(t) -> the Cache Rank
         self.io.send(kv_t)
+        self.packs += 1
         return self.out
 
     def finish(self) -> None:
-        """Drain: take every selection the Cache Rank sent (it sends one per
-        pack plus the first), so no receive is left posted."""
-        self._install()
+        """Drain: take every selection the Cache Rank sent -- one per pack plus
+        the first -- so no send is left waiting on the Cache Rank's side (with
+        'reuse' some were skipped during the steps)."""
+        while self.received < self.packs + 1:
+            self._install()

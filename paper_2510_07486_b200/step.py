@@ -49,17 +49,23 @@ class DecodeStep:
         self.window = torch.empty(B, self.n_q, W, D, dtype=window_dtype, device=dev)
         self.q = torch.empty(B, self.n_q, D, dtype=torch.bfloat16, device=dev)
         self.k_cache = torch.empty(B, hn, L, D, dtype=torch.bfloat16, device=dev)
-        self.v_cache = torch.empty(B, hn, L, D, dtype=torch.bfloat16, device=dev)
+        # absorbed MLA (v_head_dim < head_dim): the values are the latent part of
+        # the key rows -- one cache, read once
+        self.mla = bool(cfg.v_head_dim) and cfg.v_head_dim != D
+        self.dv = cfg.v_head_dim or D
+        self.v_cache = (self.k_cache if self.mla else
+                        torch.empty(B, hn, L, D, dtype=torch.bfloat16, device=dev))
         self.seq_lens = torch.full((B,), L, dtype=torch.int32, device=dev)
         self.q_hat = torch.empty(B, self.n_q, D, dtype=torch.float32, device=dev)
         self.sel_idx = torch.empty(B, hn, cfg.top_k, dtype=torch.int32, device=dev)
-        self.out = torch.empty(B, self.n_q, D, dtype=torch.float32, device=dev)
+        self.out = torch.empty(B, self.n_q, self.dv, dtype=torch.float32, device=dev)
         self.dev_flags = torch.zeros(1, dtype=torch.int32, device=dev)
         self.scores = (torch.empty(B, hn, L, dtype=torch.float32, device=dev)
                        if keep_scores else None)
         self.p_pred = predict_params(self.window, eps, flags, 0)
         self.p_sel = select_params(self.q_hat, self.k_cache, cfg.top_k)
-        self.p_dec = decode_params(self.q, self.k_cache, self.v_cache, cfg.top_k, n_fresh)
+        self.p_dec = decode_params(self.q, self.k_cache, self.v_cache, cfg.top_k, n_fresh,
+                                   v_head_dim=cfg.v_head_dim if self.mla else 0)
         self.ws_sel = torch.empty(max(score_select_workspace(self.p_sel), 256), dtype=torch.uint8,
                                   device=dev)
         self.ws_dec = torch.zeros(max(sparse_decode_workspace(self.p_dec), 256),
@@ -85,8 +91,9 @@ class DecodeStep:
             rows = slice(layer * B, (layer + 1) * B)
             synth.fill_kv_device(self.k_cache[rows], sd, synth.STREAM_K, self.b0, self.h0,
                                  cfg.n_kv_heads)
-            synth.fill_kv_device(self.v_cache[rows], sd, synth.STREAM_V, self.b0, self.h0,
-                                 cfg.n_kv_heads)
+            if not self.mla:
+                synth.fill_kv_device(self.v_cache[rows], sd, synth.STREAM_V, self.b0, self.h0,
+                                     cfg.n_kv_heads)
             if self.window.dtype == torch.float32:
                 synth.fill_query_device(self.window[rows], self.q[rows].view(torch.int16), sd,
                                         self.b0, self.q0, cfg.n_q_heads)

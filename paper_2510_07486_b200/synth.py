@@ -260,6 +260,10 @@ def fill_query_device(window, q, seed: int, b0: int = 0, h0: int = 0,
 # Qwen3-8B per-layer parameters (Table 1, head_dim 128): q/o 4096x4096,
 # k/v 4096x1024, MLP 3 x 4096x12288 -> 192.9 M params, 386 MB bf16.
 QWEN3_8B_LAYER_PARAMS = 2 * 4096 * 4096 + 2 * 4096 * 1024 + 3 * 4096 * 12288
+# Qwen3-32B (Table 1, head_dim 128): q/o 5120x8192, k/v 5120x1024, MLP
+# 3 x 5120x25600 -> 487.6 M params, 975 MB bf16 per layer (1/P of it per GPU
+# under P-way tensor parallelism)
+QWEN3_32B_LAYER_PARAMS = 2 * 5120 * 8192 + 2 * 5120 * 1024 + 3 * 5120 * 25600
 
 
 def synthetic_forward(weights, sink, stream=None) -> None:

@@ -89,8 +89,8 @@ def test_score_select_validation_and_workspace(L):
     assert call(p, ws=FAKE + 16) == 4                          # workspace must be 256-B aligned
     assert call(_sel(n_q_heads=30)) == 2
     assert call(_sel(top_k=0)) == 2
-    assert call(_sel(n_q_heads=512)) == 3                      # G = 64 (not built)
-    assert call(_sel(head_dim=256, k_stride_t=256)) == 3
+    assert call(_sel(n_q_heads=2048)) == 3                     # G = 256 (not built)
+    assert call(_sel(head_dim=96, k_stride_t=96)) == 3          # head_dim 96 (not built)
     assert call(_sel(aggregation=2)) == 1
     assert call(_sel(k_stride_t=100)) == 2                     # shorter than a row
     assert call(_sel(k_stride_t=132)) == 1                     # not a multiple of 8 elements
@@ -102,7 +102,7 @@ def _dec(**kw):
     d = dict(batch=2, n_q_heads=32, n_kv_heads=8, head_dim=128, top_k=64, n_fresh=1,
              max_seq_len=1024, sm_scale=128 ** -0.5, k_stride_b=8 * 1024 * 128, k_stride_h=1024 * 128,
              k_stride_t=128, v_stride_b=8 * 1024 * 128, v_stride_h=1024 * 128, v_stride_t=128,
-             out_stride_b=0, out_stride_h=0)
+             out_stride_b=0, out_stride_h=0, v_head_dim=0)
     d.update(kw)
     return asp.DecodeParams(*[d[f] for f, _ in asp.DecodeParams._fields_])
 
@@ -124,6 +124,15 @@ def test_sparse_decode_validation_and_workspace(L):
     assert call(_dec(n_fresh=-1)) == 2
     assert call(_dec(n_q_heads=12)) == 2
     assert call(_dec(head_dim=80, k_stride_t=80, v_stride_t=80)) == 3
+    # v_head_dim (ABI 2): > head_dim is a shape error; MLA 576 / 512 at G = 4 is built
+    assert call(_dec(v_head_dim=256)) == 2
+    mla = _dec(n_q_heads=32, n_kv_heads=8, head_dim=576, v_head_dim=512, k_stride_t=576,
+               v_stride_t=576, k_stride_b=8 * 1024 * 576, k_stride_h=1024 * 576,
+               v_stride_b=8 * 1024 * 576, v_stride_h=1024 * 576)
+    # split-K partials of Dv = 512 values: [B][Hq][1][512 + 2] fp32
+    assert L.asyncspade_sparse_decode_workspace(ctypes.byref(mla)) >= 2 * 32 * 514 * 4
+    assert L.asyncspade_sparse_decode_workspace(ctypes.byref(_dec(head_dim=576, v_head_dim=448,
+                                                                  k_stride_t=576, v_stride_t=576))) == 0
     assert call(_dec(v_stride_h=1004)) == 1
     assert call(_dec(sm_scale=float("nan"))) == 1
     assert call(_dec(max_seq_len=0)) == 2

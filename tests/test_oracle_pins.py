@@ -537,3 +537,28 @@ def test_ar1_prediction_beats_random_selection():
     rnd = np.mean([len(np.intersect1d(np.sort(rng.choice(N, k, replace=False)), i_true[b, h])) / k
                    for b in range(B) for h in range(Hq)])
     assert abs(rnd - k / N) < 0.03, rnd
+
+
+def test_decode_values_narrower_than_keys_absorbed_mla():
+    """NEXT-3 absorbed MLA: the value of a token is the first Dv
+    dims of its key row (the latent); the oracle's decode over V narrower than
+    K equals numpy softmax attention with logits over all D key dims and the
+    weighted sum over the Dv value dims."""
+    rng = np.random.default_rng(57)
+    B, Hq, Hkv, D, Dv, L = 2, 4, 1, 96, 64, 40
+    q = synth.f32_to_bf16_bits(rng.standard_normal((B, Hq, D)).astype(np.float32))
+    K = synth.f32_to_bf16_bits(rng.standard_normal((B, Hkv, L, D)).astype(np.float32))
+    V = np.ascontiguousarray(K[..., :Dv])
+    idx = np.stack([np.stack([np.sort(rng.choice(L - 1, 9, replace=False))]) for _ in range(B)]).astype(np.int32)
+    out = oracle.sparse_decode(q, K, V, idx, [L] * B, n_fresh=1, sm_scale=0.11)
+    assert out.shape == (B, Hq, Dv)
+    for b in range(B):
+        toks = list(idx[b, 0]) + [L - 1]
+        Kf = synth.bf16_bits_to_f32(K[b, 0]).astype(np.float64)
+        for hq in range(Hq):
+            qf = synth.bf16_bits_to_f32(q[b, hq]).astype(np.float64)
+            l = 0.11 * (Kf[toks] @ qf)
+            p = np.exp(l - l.max())
+            p /= p.sum()
+            ref = p @ Kf[toks, :Dv]
+            np.testing.assert_allclose(out[b, hq], ref, rtol=1e-6, atol=1e-7)

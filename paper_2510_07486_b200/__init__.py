@@ -227,7 +227,28 @@ def _workspace(nbytes: int, device) -> torch.Tensor:
     return torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
 
 
+# NVTX ranges per entry point (SURVEY §5 profiling), on when ASP_NVTX=1: ncu
+# --nvtx / nsys timelines then show each call; off by default (host-side cost).
+_NVTX = os.environ.get("ASP_NVTX", "0") == "1"
+
+
+def _nvtx(fn):
+    if not _NVTX:
+        return fn
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(*a, **kw):
+        torch.cuda.nvtx.range_push(fn.__name__)
+        try:
+            return fn(*a, **kw)
+        finally:
+            torch.cuda.nvtx.range_pop()
+    return wrapped
+
+
 # --------------------------------------------------------------------------- entry points
+@_nvtx
 def append(q_t: torch.Tensor, q_window: torch.Tensor | None, ring_slot: int, *,
            q_cur: torch.Tensor | None = None, k_new: torch.Tensor | None = None,
            v_new: torch.Tensor | None = None, k_cache: torch.Tensor | None = None,
@@ -258,6 +279,7 @@ def append(q_t: torch.Tensor, q_window: torch.Tensor | None, ring_slot: int, *,
            "asyncspade_append")
 
 
+@_nvtx
 def predict_query(q_window: torch.Tensor, q_hat: torch.Tensor | None = None, *, eps: float = 1e-2,
                   flags: int = 0, ring_start: int = 0, dev_flags: torch.Tensor | None = None,
                   stream=None, params: PredictParams | None = None) -> torch.Tensor:
@@ -273,6 +295,7 @@ def predict_query(q_window: torch.Tensor, q_hat: torch.Tensor | None = None, *, 
     return q_hat
 
 
+@_nvtx
 def score_select(q_hat: torch.Tensor, k_cache: torch.Tensor, seq_lens: torch.Tensor, top_k: int,
                  *, sel_idx: torch.Tensor | None = None, scores: torch.Tensor | None = None,
                  workspace: torch.Tensor | None = None, aggregation: int = AGG_MAX,
@@ -299,6 +322,7 @@ def score_select(q_hat: torch.Tensor, k_cache: torch.Tensor, seq_lens: torch.Ten
     return sel_idx
 
 
+@_nvtx
 def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
                   seq_lens: torch.Tensor, sel_idx: torch.Tensor, *, n_fresh: int = 0,
                   sm_scale: float | None = None, out: torch.Tensor | None = None,
@@ -323,6 +347,7 @@ def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
     return out
 
 
+@_nvtx
 def gather_filtered(k_cache: torch.Tensor, v_cache: torch.Tensor, seq_lens: torch.Tensor,
                     sel_idx: torch.Tensor, *, n_fresh: int = 0, k_out: torch.Tensor | None = None,
                     v_out: torch.Tensor | None = None, idx_out: torch.Tensor | None = None,
@@ -361,6 +386,7 @@ def paged_kv(k_pages: torch.Tensor, block_table: torch.Tensor) -> PagedKV:
     return PagedKV(P, block_table.shape[1], n_pages)
 
 
+@_nvtx
 def score_select_paged(q_hat: torch.Tensor, k_pages: torch.Tensor, block_table: torch.Tensor,
                        seq_lens: torch.Tensor, top_k: int, max_seq_len: int, *,
                        sel_idx: torch.Tensor | None = None, scores: torch.Tensor | None = None,
@@ -389,6 +415,7 @@ def score_select_paged(q_hat: torch.Tensor, k_pages: torch.Tensor, block_table: 
     return sel_idx
 
 
+@_nvtx
 def sparse_decode_paged(q: torch.Tensor, k_pages: torch.Tensor, v_pages: torch.Tensor,
                         block_table: torch.Tensor, seq_lens: torch.Tensor, sel_idx: torch.Tensor,
                         max_seq_len: int, *, n_fresh: int = 0, sm_scale: float | None = None,
@@ -437,6 +464,7 @@ def page_pool(cache: torch.Tensor, page_size: int, generator: torch.Generator | 
 
 
 # --------------------------------------------------------------------------- Quest comparator
+@_nvtx
 def quest_summarize(k_cache: torch.Tensor, seq_lens: torch.Tensor, page_size: int, top_k: int,
                     n_q_heads: int, *, meta: torch.Tensor | None = None,
                     stream=None) -> torch.Tensor:
@@ -452,6 +480,7 @@ def quest_summarize(k_cache: torch.Tensor, seq_lens: torch.Tensor, page_size: in
     return meta
 
 
+@_nvtx
 def quest_select(q: torch.Tensor, meta: torch.Tensor, k_cache: torch.Tensor,
                  seq_lens: torch.Tensor, top_k: int, page_size: int, *,
                  sel_idx: torch.Tensor | None = None, workspace: torch.Tensor | None = None,

@@ -11,8 +11,9 @@ bool aligned16(const void *ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u
 // the tensor-core kernels (score.cu, decode.cu): head_dim 64 / 128, G <= 32
 bool group_ok(int G) { return G == 1 || G == 2 || G == 4 || G == 8 || G == 16 || G == 32; }
 bool dim_ok(int D) { return D == 64 || D == 128; }
-bool tc_select_ok(const asp_select_params *p) {
-    return dim_ok(p->head_dim) && group_ok(p->n_q_heads / p->n_kv_heads);
+bool tc_select_ok(const asp_select_params *p) {     // score.cu also runs G = 64 (MQA)
+    const int G = p->n_q_heads / p->n_kv_heads;
+    return dim_ok(p->head_dim) && (group_ok(G) || G == 64);
 }
 int v_dim_of(const asp_decode_params *p) { return p->v_head_dim ? p->v_head_dim : p->head_dim; }
 bool tc_decode_ok(const asp_decode_params *p) {

@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                  const asp_bf16 *__restrict__ k_cache, const asp_bf16 *__restrict__ v_cache,
                  const int32_t *__restrict__ seq_lens, const int32_t *__restrict__ sel_idx,
-                 float *__restrict__ partials, int n_splits, PagedArgs pg) {
+                 float *__restrict__ partials, float *__restrict__ out, int n_splits, PagedArgs pg) {
     using C = DCfg<D, G>;
     constexpr int kGR = C::kGR;
     extern __shared__ unsigned char smem_raw[];
@@ -546,6 +546,21 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             const Item it = item(i);
             const int b = it.row / Hkv, h = it.row % Hkv;
             const int d = quad * 32 + lane;
+            if (n_splits == 1) {
+                // a row of one chunk: out = o / l, exactly what the combine's merge
+                // of a single partial gives (exp2f(0) = 1, fmaf(x, 1, 0) = x)
+                const int64_t osb = p.out_stride_b ? p.out_stride_b : (int64_t)Hq * D;
+                const int64_t osh = p.out_stride_h ? p.out_stride_h : (int64_t)D;
+#pragma unroll
+                for (int g = 0; g < G; g++) {
+                    float L = 0.0f;
+#pragma unroll
+                    for (int w = 0; w < 4; w++) L += s_wsum[(slot * 4 + w) * kGR + g];
+                    const float O = __fadd_rn(__uint_as_float(r[g]), __uint_as_float(r[G + g]));
+                    if (d < D) out[b * osb + (int64_t)(h * G + g) * osh + d] = (L > 0.0f) ? O / L : 0.0f;
+                }
+                return;
+            }
 #pragma unroll
             for (int g = 0; g < G; g++) {
                 // partials are read back by the combine kernel right after:
@@ -585,15 +600,36 @@ decode_combine_kernel(asp_decode_params p, const float *__restrict__ partials,
     asp::pdl_wait();
     asp::pdl_trigger();
     const float *src = partials + ((size_t)b * p.n_q_heads + hq) * n_splits * (D + 2);
+    // chunk order is the merge order; the loads of 8 chunks are issued together
+    // (long-CoT rows have 128 chunks: one dependent L2 round trip each would
+    // dominate), the arithmetic stays sequential in s
+    constexpr int kB = 16;
+    // M: every warp reduces all chunk maxima lane-parallel (fmax is exact and
+    // order-free), so long-CoT rows (128 chunks) pay 4 round trips, not 128
     float M = -INFINITY;
-    for (int s = 0; s < n_splits; s++) M = fmaxf(M, src[(size_t)s * (D + 2)]);
+    for (int s = (int)(threadIdx.x & 31); s < n_splits; s += 32) M = fmaxf(M, src[(size_t)s * (D + 2)]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     float L = 0.0f, O = 0.0f;
     if (M != -INFINITY) {
-        for (int s = 0; s < n_splits; s++) {
-            const float *ps = src + (size_t)s * (D + 2);
-            const float a = exp2f(ps[0] - M);
-            L = fmaf(ps[1], a, L);
-            O = fmaf(ps[2 + d], a, O);
+        for (int s0 = 0; s0 < n_splits; s0 += kB) {
+            float m[kB], l[kB], o[kB];
+#pragma unroll
+            for (int u = 0; u < kB; u++) {
+                const bool ok = s0 + u < n_splits;
+                const float *ps = src + (size_t)(ok ? s0 + u : s0) * (D + 2);
+                m[u] = ps[0];
+                l[u] = ps[1];
+                o[u] = ps[2 + d];
+            }
+#pragma unroll
+            for (int u = 0; u < kB; u++) {
+                if (s0 + u < n_splits) {
+                    const float a = exp2f(m[u] - M);
+                    L = fmaf(l[u], a, L);
+                    O = fmaf(o[u], a, O);
+                }
+            }
         }
     }
     const int64_t osb = p.out_stride_b ? p.out_stride_b : (int64_t)p.n_q_heads * D;
@@ -629,8 +665,8 @@ cudaError_t launch(const asp_decode_params &p, const asp_bf16 *q, const asp_bf16
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
     e = asp_launch(kern, dim3(grid), dim3(kThreads), C::kSmemBytes, s, 1, p, q, k, v, seq_lens,
-                   idx, partials, ns, pg);
-    if (e != cudaSuccess) return e;
+                   idx, partials, out, ns, pg);
+    if (e != cudaSuccess || ns == 1) return e;            // one chunk: written directly
     return asp_launch(decode_combine_kernel<D>, dim3(p.n_q_heads, p.batch), dim3(D), 0, s, 1, p,
                       (const float *)partials, out, ns);
 }

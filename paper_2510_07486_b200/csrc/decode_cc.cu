@@ -29,6 +29,9 @@ struct DccCfg {
     static constexpr int kRowV = DV + 8;
     static constexpr int kTPH = kThreads / G;                    // threads per head (P.V)
     static constexpr int kDPT = DV / kTPH;                       // output dims per thread
+    // ... in kNG groups of kVW contiguous dims (vector loads of V)
+    static constexpr int kVW = kDPT % 8 == 0 ? 8 : kDPT % 4 == 0 ? 4 : 2;
+    static constexpr int kNG = kDPT / kVW;
     static constexpr int kLG = G < 8 ? G : 8;                    // logit head groups
     static constexpr int kLHPT = G / kLG;                        // logit heads per thread
     static constexpr int kQBytes = G * DK * 4;
@@ -193,7 +196,8 @@ decode_cc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                 ss[tid] = sc;
             }
             __syncthreads();
-            // ---- o[og][od + kTPH e] = o * scale + sum_j w_j V_j
+            // ---- o[og][dims of group e] = o * scale + sum_j w_j V_j; thread od owns
+            // the kVW-dim groups (od + kTPH e) (vector loads of the V rows)
             {
                 const asp_bf16 *vt = v_from_k ? kt : sv + buf * (kSub * C::kRowV);
                 const int vrow = v_from_k ? C::kRowK : C::kRowV;
@@ -203,9 +207,26 @@ decode_cc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                 for (int j = 0; j < kSub; j++) {
                     const float w = sp[og * kSub + j];
                     if (w == 0.0f) continue;                      // uniform per head group
-                    const asp_bf16 *vr = vt + j * vrow + od;
+                    const asp_bf16 *vr = vt + j * vrow;
 #pragma unroll
-                    for (int e = 0; e < C::kDPT; e++) acc[e] = fmaf(w, asp::bf16f(vr[C::kTPH * e]), acc[e]);
+                    for (int e = 0; e < C::kNG; e++) {
+                        const asp_bf16 *vg = vr + (od + C::kTPH * e) * C::kVW;
+                        uint32_t w4[C::kVW / 2];
+                        if constexpr (C::kVW == 8) {
+                            const uint4 x = *reinterpret_cast<const uint4 *>(vg);
+                            w4[0] = x.x; w4[1] = x.y; w4[2] = x.z; w4[3] = x.w;
+                        } else if constexpr (C::kVW == 4) {
+                            const uint2 x = *reinterpret_cast<const uint2 *>(vg);
+                            w4[0] = x.x; w4[1] = x.y;
+                        } else {
+                            w4[0] = *reinterpret_cast<const uint32_t *>(vg);
+                        }
+#pragma unroll
+                        for (int v = 0; v < C::kVW / 2; v++) {
+                            acc[e * C::kVW + 2 * v] = fmaf(w, asp::bf16lo(w4[v]), acc[e * C::kVW + 2 * v]);
+                            acc[e * C::kVW + 2 * v + 1] = fmaf(w, asp::bf16hi(w4[v]), acc[e * C::kVW + 2 * v + 1]);
+                        }
+                    }
                 }
             }
             __syncthreads();                                      // sub-tile buffers reusable
@@ -213,7 +234,8 @@ decode_cc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
         // ---- the chunk's partial: m (log2 units), l, o for every head
         float *dst = partials + (((size_t)b * Hq + (size_t)h * G + og) * n_splits + chunk) * (DV + 2);
 #pragma unroll
-        for (int e = 0; e < C::kDPT; e++) dst[2 + od + C::kTPH * e] = any ? acc[e] : 0.0f;
+        for (int e = 0; e < C::kDPT; e++)
+            dst[2 + (od + C::kTPH * (e / C::kVW)) * C::kVW + e % C::kVW] = any ? acc[e] : 0.0f;
         if (od == 0) {
             dst[0] = any ? sm[og] : -INFINITY;
             dst[1] = any ? sl[og] : 0.0f;
@@ -229,12 +251,14 @@ __global__ void decode_cc_combine_kernel(asp_decode_params p, int dv, const floa
     asp::pdl_trigger();
     const float *src = partials + ((size_t)b * p.n_q_heads + hq) * n_splits * (dv + 2);
     float M = -INFINITY;
+#pragma unroll 8
     for (int s = 0; s < n_splits; s++) M = fmaxf(M, src[(size_t)s * (dv + 2)]);
     const int64_t osb = p.out_stride_b ? p.out_stride_b : (int64_t)p.n_q_heads * dv;
     const int64_t osh = p.out_stride_h ? p.out_stride_h : (int64_t)dv;
     for (int d = threadIdx.x; d < dv; d += blockDim.x) {
         float L = 0.0f, O = 0.0f;
         if (M != -INFINITY) {
+#pragma unroll 8
             for (int s = 0; s < n_splits; s++) {
                 const float *ps = src + (size_t)s * (dv + 2);
                 const float a = exp2f(ps[0] - M);

@@ -71,15 +71,21 @@ struct Cfg {
     static constexpr int kStageBytes = kTileM * D * 2;
     static constexpr int kBRegionBytes = N * 128;
     static constexpr int kBSlotBytes = kRegions * kBRegionBytes;
-    // accumulator stages: 6, or as many as fit the 512 TMEM columns (G = 16: 5, G = 32: 2)
-    static constexpr int kAcc = (2 * ::kAcc * N) <= 512 ? ::kAcc : 512 / (2 * N);
+    // accumulation chains per tile: even / odd k-steps in two TMEM halves (short
+    // MMAs, latency-bound chains), one chain when N > 96 (G = 64: an N = 192 MMA
+    // is long enough, and two halves would leave room for a single stage)
+    static constexpr int kHalves = N <= 96 ? 2 : 1;
+    // accumulator stages: 6, or as many as fit the 512 TMEM columns (G = 16: 5,
+    // G = 32: 2, G = 64: 2)
+    static constexpr int kAcc = (kHalves * ::kAcc * N) <= 512 ? ::kAcc : 512 / (kHalves * N);
     // K ring: 6 stages, fewer when the B-operand ring needs the room (G = 32: 5)
     static constexpr int kStages =
         (1024 + ::kStages * kTileM * D * 2 + kBSlots * (D / 64) * N * 128 + 256) <= 227 * 1024
             ? ::kStages
             : (227 * 1024 - 1024 - kBSlots * (D / 64) * N * 128 - 256) / (kTileM * D * 2);
-    static constexpr uint32_t kTmemCols = (2 * kAcc * N) <= 64 ? 64 : (2 * kAcc * N) <= 128 ? 128
-                                          : (2 * kAcc * N) <= 256 ? 256 : 512;
+    static constexpr uint32_t kTmemCols = (kHalves * kAcc * N) <= 64 ? 64
+                                          : (kHalves * kAcc * N) <= 128 ? 128
+                                          : (kHalves * kAcc * N) <= 256 ? 256 : 512;
     static constexpr int kSmemBytes = 1024 /*align slack*/ + Cfg::kStages * kStageBytes +
                                       kBSlots * kBSlotBytes + 256 /*barriers*/;
 };
@@ -431,7 +437,9 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
                 int gs[kGroup], ga[kGroup], ng = 0;
                 // (a group never needs more accumulator stages than exist: every
                 // tile of it waits for its stage before any of them is issued)
-                constexpr int kGroupMax = C::kAcc < kGroup ? C::kAcc : kGroup;
+                // (one-chain tiles -- G = 64 -- are long MMAs on their own: issue each as
+                // soon as its stage and an accumulator are free, never wait for a group)
+                constexpr int kGroupMax = C::kHalves == 1 ? 1 : (C::kAcc < kGroup ? C::kAcc : kGroup);
                 while (ng < kGroupMax && i < it.end && it.row == row) {
                     PWAIT(pm_full, mbar_wait(full_bar(s), ph));
                     PWAIT(pm_tempty, mbar_wait(tempty_bar(a), aph ^ 1));
@@ -454,7 +462,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
 #pragma unroll
                 for (int t = 0; t < kGroup; t++) {
                     adesc[t] = desc_sw128_kmajor(stage0 + gs[t < ng ? t : 0] * C::kStageBytes);
-                    dcol[t] = tmem_base + ga[t < ng ? t : 0] * (2 * N);
+                    dcol[t] = tmem_base + ga[t < ng ? t : 0] * (C::kHalves * N);
                 }
                 const uint64_t bdesc0 = desc_sw128_kmajor(b_base);
                 auto issue = [&](auto NG) {
@@ -464,12 +472,16 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
                         const uint64_t aoff = (uint64_t)((r * (kTileM * 128) + ko) >> 4);
                         const uint64_t bdesc = bdesc0 + (uint64_t)((r * C::kBRegionBytes + ko) >> 4);
 #pragma unroll
-                        for (int t = 0; t < decltype(NG)::value; t++)
-                            mma_bf16_warp(dcol[t] + (kk & 1) * N, adesc[t] + aoff, bdesc, idesc,
-                                          kk > 1 ? 1u : 0u);
+                        for (int t = 0; t < decltype(NG)::value; t++) {
+                            if constexpr (C::kHalves == 2)
+                                mma_bf16_warp(dcol[t] + (kk & 1) * N, adesc[t] + aoff, bdesc, idesc,
+                                              kk > 1 ? 1u : 0u);
+                            else
+                                mma_bf16_warp(dcol[t], adesc[t] + aoff, bdesc, idesc, kk > 0 ? 1u : 0u);
+                        }
                     }
                 };
-                if (D == 128 && ng == 3)
+                if (D == 128 && ng == 3 && C::kHalves == 2)
                     mma_group3_d128(adesc[0], adesc[1], adesc[2], bdesc0, dcol[0], dcol[1], dcol[2],
                                     idesc, (uint64_t)(C::kBRegionBytes >> 4), (uint32_t)N);
                 else if (ng == kGroup) issue(std::integral_constant<int, kGroup>{});
@@ -553,9 +565,28 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
             const int row = it.row, j = it.j;
             PWAIT(pe_full, mbar_wait(tfull_bar(a), aph));
             tc_fence_after();
-            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + a * (2 * N);
-            float v[N];                                 // even + odd k-step halves (fixed order)
-            if constexpr (N == 32) {
+            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + a * (C::kHalves * N);
+            float v[N <= 96 ? N : 32];                  // even + odd k-step halves (fixed order)
+            float s_big = 0.0f;                         // G >= 64: reduced block by block
+            if constexpr (N > 96) {
+                // one chain; heads in blocks of 32: s_g = (hi_g + mid_g) + lo_g, then
+                // the group reduction block by block (fixed order)
+#pragma unroll 1
+                for (int gb = 0; gb < G / 32; gb++) {
+                    uint32_t rh[32], rm[32], rl[32];
+                    tmem_ld32(taddr + 32 * gb, rh);
+                    tmem_ld32(taddr + G + 32 * gb, rm);
+                    tmem_ld32(taddr + 2 * G + 32 * gb, rl);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int g = 0; g < 32; g++) {
+                        const float sg = __fadd_rn(__fadd_rn(__uint_as_float(rh[g]), __uint_as_float(rm[g])),
+                                                   __uint_as_float(rl[g]));
+                        s_big = (gb == 0 && g == 0) ? sg
+                              : (p.aggregation == ASP_AGG_SUM ? __fadd_rn(s_big, sg) : fmaxf(s_big, sg));
+                    }
+                }
+            } else if constexpr (N == 32) {
                 uint32_t r0[32], r1[32];
                 tmem_ld32(taddr, r0);
                 tmem_ld32(taddr + N, r1);
@@ -602,11 +633,13 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty_bar(a));
-            float s = 0.0f;
+            float s = s_big;
+            if constexpr (N <= 96) {
 #pragma unroll
-            for (int g = 0; g < G; g++) {
-                const float sg = N == 96 ? v[g] : __fadd_rn(__fadd_rn(v[g], v[G + g]), v[2 * G + g]);
-                s = g == 0 ? sg : (p.aggregation == ASP_AGG_SUM ? __fadd_rn(s, sg) : fmaxf(s, sg));
+                for (int g = 0; g < G; g++) {
+                    const float sg = N == 96 ? v[g] : __fadd_rn(__fadd_rn(v[g], v[G + g]), v[2 * G + g]);
+                    s = g == 0 ? sg : (p.aggregation == ASP_AGG_SUM ? __fadd_rn(s, sg) : fmaxf(s, sg));
+                }
             }
             const int tok = j * kTileM + quad * 32 + lane;
             const int len = it.len_of(row);
@@ -701,6 +734,7 @@ cudaError_t asp_launch_score(const asp_select_params &p, const float *q_hat,
     ASP_CASE(64, 1) ASP_CASE(64, 2) ASP_CASE(64, 4) ASP_CASE(64, 8)
     ASP_CASE(128, 1) ASP_CASE(128, 2) ASP_CASE(128, 4) ASP_CASE(128, 8)
     ASP_CASE(64, 16) ASP_CASE(128, 16) ASP_CASE(64, 32) ASP_CASE(128, 32)
+    ASP_CASE(64, 64) ASP_CASE(128, 64)
 #undef ASP_CASE
     return cudaErrorInvalidValue;
 }

@@ -153,6 +153,52 @@ class CacheRank:
         self.send_selection(keep)
 
 
+class _StagedReceiver:
+    """gloo: a background thread keeps a receive of the next selection posted
+    (gloo completes a receive only inside wait(), so is_completed() cannot be
+    polled) and queues the host copies; done() / finish() mirror _Pending."""
+
+    def __init__(self, io: "Transport", shapes):
+        import queue
+        import threading
+        self.io, self.q = io, queue.Queue()
+        self.sizes = [int(torch.Size(sh).numel()) * es for sh, es in shapes]
+        self.stop = False
+        # one credit per selection the Cache Rank owes (the first, then one per
+        # pack): the thread never posts a receive nobody will answer
+        self.credits = threading.Semaphore(1)
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+
+    def expect_one(self) -> None:
+        self.credits.release()
+
+    def close(self) -> None:
+        self.stop = True
+        self.credits.release()
+        self.th.join(timeout=30)
+
+    def _run(self):
+        while True:
+            self.credits.acquire()
+            if self.stop:
+                return
+            hs = []
+            for n in self.sizes:
+                h = torch.empty(n, dtype=torch.uint8)
+                dist.recv(h, self.io.peer, group=self.io.recv_group)
+                hs.append(h)
+            self.q.put(hs)
+
+    def done(self) -> bool:
+        return not self.q.empty()
+
+    def take(self, targets) -> None:
+        hs = self.q.get()
+        for t, h in zip(targets, hs):
+            t.view(torch.uint8).view(-1).copy_(h.to(t.device))
+
+
 class InferenceRank:
     """Attends over the received selection plus its own newest token; sends
     each step's (q_t, k_t, v_t) to the Cache Rank.  Two compact caches: the
@@ -181,17 +227,28 @@ class InferenceRank:
         self.received = 0                  # selections installed so far
         self.used = []                     # per step: which selection (0-based) was used
         self.packs = 0                     # packs sent (the Cache Rank answers each)
+        self.rx = None
+        if self.io.staged:
+            self.rx = _StagedReceiver(self.io, [(t.shape, t.element_size())
+                                                for t in (self.k_c[0], self.v_c[0], self.idx[0])])
         self._post()
 
     def _post(self) -> None:
         nxt = 1 if self.cur == 0 else 0
         self.spare = nxt
-        self.pending = [self.io.irecv(self.k_c[nxt]), self.io.irecv(self.v_c[nxt]),
-                        self.io.irecv(self.idx[nxt])]
+        if self.rx is None:
+            self.pending = [self.io.irecv(self.k_c[nxt]), self.io.irecv(self.v_c[nxt]),
+                            self.io.irecv(self.idx[nxt])]
+
+    def _arrived(self) -> bool:
+        return self.rx.done() if self.rx is not None else all(pr.done() for pr in self.pending)
 
     def _install(self) -> None:
-        for pr in self.pending:
-            pr.finish()
+        if self.rx is not None:
+            self.rx.take([self.k_c[self.spare], self.v_c[self.spare], self.idx[self.spare]])
+        else:
+            for pr in self.pending:
+                pr.finish()
         self.cur = self.spare
         self.received += 1
         self._post()
@@ -201,7 +258,7 @@ class InferenceRank:
         [2, B, Hkv, D] (the new token).  Returns the attention output."""
         if self.cur < 0 or self.policy == "wait":
             self._install()                            # sel(t): wait for it
-        while all(pr.done() for pr in self.pending):   # reuse: take the newest arrived
+        while self._arrived():                         # reuse: take the newest arrived
             self._install()
         self.used.append(self.received - 1)
         c = self.cur
@@ -213,6 +270,8 @@ class InferenceRank:
         self.io.send(q_t)                              # pack(t) -> the Cache Rank
         self.io.send(kv_t)
         self.packs += 1
+        if self.rx is not None:
+            self.rx.expect_one()                       # sel(t + 1) will answer it
         return self.out
 
     def finish(self) -> None:
@@ -221,3 +280,5 @@ class InferenceRank:
         'reuse' some were skipped during the steps)."""
         while self.received < self.packs + 1:
             self._install()
+        if self.rx is not None:
+            self.rx.close()

@@ -670,7 +670,7 @@ def _dual_rank(tmp_path, *args):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = str(tmp_path / "dual.npz")
     r = subprocess.run([sys.executable, os.path.join(root, "scripts", "disagg_two_rank.py"), out,
-                        *args], capture_output=True, text=True, timeout=400, cwd=root)
+                        *args], capture_output=True, text=True, timeout=240, cwd=root)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     return dict(np.load(out))
 
@@ -713,8 +713,11 @@ def test_dual_rank_late_cache_rank_reuses_previous_selection(tmp_path):
     actually used."""
     d = _dual_rank(tmp_path, "--policy", "reuse", "--late", "1", "--steps", "5")
     used = d["used"].tolist()
-    assert used[:2] == [0, 1] and used[2] == 1, used
-    assert used[-1] >= 3 and all(b >= a for a, b in zip(used, used[1:])), used
+    # step t can use at most sel(t); sel(2) is half a second late, so step 2
+    # attends with an older one; selections are taken in order, newest first
+    assert used[0] == 0 and all(u <= t for t, u in enumerate(used)), used
+    assert used[2] <= 1, used
+    assert all(b >= a for a, b in zip(used, used[1:])) and used[-1] >= 2, used
     _dual_rank_oracle_check(d)
 
 

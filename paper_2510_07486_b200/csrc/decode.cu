@@ -600,36 +600,20 @@ decode_combine_kernel(asp_decode_params p, const float *__restrict__ partials,
     asp::pdl_wait();
     asp::pdl_trigger();
     const float *src = partials + ((size_t)b * p.n_q_heads + hq) * n_splits * (D + 2);
-    // chunk order is the merge order; the loads of 8 chunks are issued together
-    // (long-CoT rows have 128 chunks: one dependent L2 round trip each would
-    // dominate), the arithmetic stays sequential in s
-    constexpr int kB = 16;
-    // M: every warp reduces all chunk maxima lane-parallel (fmax is exact and
-    // order-free), so long-CoT rows (128 chunks) pay 4 round trips, not 128
+    // chunk order is the merge order; unrolled by 8 so the loads of 8 chunks
+    // are in flight together (long-CoT rows have 128 chunks: one dependent L2
+    // round trip each would dominate), the arithmetic stays sequential in s
     float M = -INFINITY;
-    for (int s = (int)(threadIdx.x & 31); s < n_splits; s += 32) M = fmaxf(M, src[(size_t)s * (D + 2)]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+#pragma unroll 8
+    for (int s = 0; s < n_splits; s++) M = fmaxf(M, src[(size_t)s * (D + 2)]);
     float L = 0.0f, O = 0.0f;
     if (M != -INFINITY) {
-        for (int s0 = 0; s0 < n_splits; s0 += kB) {
-            float m[kB], l[kB], o[kB];
-#pragma unroll
-            for (int u = 0; u < kB; u++) {
-                const bool ok = s0 + u < n_splits;
-                const float *ps = src + (size_t)(ok ? s0 + u : s0) * (D + 2);
-                m[u] = ps[0];
-                l[u] = ps[1];
-                o[u] = ps[2 + d];
-            }
-#pragma unroll
-            for (int u = 0; u < kB; u++) {
-                if (s0 + u < n_splits) {
-                    const float a = exp2f(m[u] - M);
-                    L = fmaf(l[u], a, L);
-                    O = fmaf(o[u], a, O);
-                }
-            }
+#pragma unroll 8
+        for (int s = 0; s < n_splits; s++) {
+            const float *ps = src + (size_t)s * (D + 2);
+            const float a = exp2f(ps[0] - M);
+            L = fmaf(ps[1], a, L);
+            O = fmaf(ps[2 + d], a, O);
         }
     }
     const int64_t osb = p.out_stride_b ? p.out_stride_b : (int64_t)p.n_q_heads * D;

@@ -89,8 +89,8 @@ cudaError_t asp_launch_select(const asp_select_params &p, const float *scores,
                               bool discard_scores, cudaStream_t s) {
     const long L = p.max_seq_len;
     const long rows = (long)p.batch * p.n_kv_heads;
-    // Cluster size: segments of <= 64k keys (one emission round, bitmaps in
-    // shared memory), then split further while the rows would leave SMs idle,
+    // Cluster size (measured on B200): segments of <= 64k keys, then split
+    // further only while the rows could not even occupy a quarter of the SMs,
     // keeping segments >= 16k keys (DSMEM merges cost more than they save on
     // shorter segments).
     const long target = asp_sm_count() / 4;

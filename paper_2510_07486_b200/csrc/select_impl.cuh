@@ -6,22 +6,17 @@ constexpr int kThreads = SEL_NT;
 constexpr int kWarps = kThreads / 32;
 constexpr int kBins = 4096;
 constexpr int kCand = 2048;                   // candidate slots per CTA
-constexpr int kRound = 65536;                 // keys per emission round (bitmap capacity)
-constexpr int kRoundChunks = kRound / 128;    // 128-key chunks per round
+constexpr int kRound = 32768;                 // keys per emission round (bitmap size)
 constexpr int kSampleChunks = 32;             // 32 x 128 consecutive keys sampled per row
 constexpr int kMaxCluster = 16;
 constexpr int kUnroll = 8;                    // 16-B loads in flight per lane (classify)
 
-// Bitmaps are in index order: word w bit j <-> key 32 w + j.  A warp reads a
-// 128-key chunk as four coalesced 128-B loads (lane l takes keys 32 j + l,
-// j = 0..3), so the ballot of load j IS bitmap word 4 * chunk + j:
-// classification costs one compare + one ballot per key and no shuffles.
 struct SelectSmem {
     uint32_t hist[kBins];
     uint32_t cand[kCand];          // candidate keys (any order)
-    uint16_t cand_idx[kCand];      // their offsets inside the round (< kRound)
-    uint32_t bm_gt[kRound / 32];   // key > T (seeded with the keys above the bracket)
-    uint32_t bm_eq[kRound / 32];   // key == T
+    uint32_t cand_idx[kCand];      // their segment offsets
+    uint32_t bm_gt[kRound / 32];
+    uint32_t bm_eq[kRound / 32];
     uint32_t n_cand;
     uint32_t warp_a[kWarps], warp_b[kWarps];
     uint32_t scan_total;
@@ -214,46 +209,6 @@ __device__ __noinline__ void cluster_counts(SelectSmem &s, int C, int n, uint32_
     }
 }
 
-// Emit the selected indices of one round from the bitmaps (bm_gt: key > T,
-// bm_eq: key == T; only the first `need` equal keys of the ROW, in index
-// order, are taken): each thread owns a run of words, a block scan of their
-// popcounts gives its output offsets, then it writes its indices in order.
-// gt_run / eq_run: keys of this row before the round (earlier cluster ranks
-// and rounds); updated.
-__device__ __forceinline__ void emit_round(SelectSmem &s, int rwords, int base_idx, uint32_t need,
-                                           uint32_t &gt_run, uint32_t &eq_run, int32_t *out) {
-    const int t = threadIdx.x;
-    const int wpt = (rwords + kThreads - 1) / kThreads;           // words per thread
-    const int wa = min(t * wpt, rwords), wb = min(wa + wpt, rwords);
-    uint32_t cgt = 0, ceq = 0;
-    for (int w = wa; w < wb; w++) {
-        cgt += __popc(s.bm_gt[w]);
-        ceq += __popc(s.bm_eq[w]);
-    }
-    uint32_t tg, te;
-    uint32_t gt_before = gt_run + block_excl_scan(s, cgt, &tg);
-    uint32_t eq_before = eq_run + block_excl_scan(s, ceq, &te);
-    for (int w = wa; w < wb; w++) {
-        const uint32_t g = s.bm_gt[w], e = s.bm_eq[w];
-        uint32_t bits = g | e;
-        while (bits) {
-            const int bit = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const int idx = base_idx + (w << 5) + bit;
-            if ((g >> bit) & 1u) {
-                out[gt_before + min(eq_before, need)] = idx;
-                gt_before++;
-            } else {
-                if (eq_before < need) out[gt_before + eq_before] = idx;
-                eq_before++;
-            }
-        }
-    }
-    gt_run += tg;
-    eq_run += te;
-    __syncthreads();                       // the bitmaps are rewritten next round
-}
-
 __global__ void __launch_bounds__(kThreads, SEL_MINB)
 select_kernel(asp_select_params p, const float *__restrict__ scores,
               const int32_t *__restrict__ seq_lens, int32_t *__restrict__ sel_idx,
@@ -289,7 +244,9 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
     const float *srow = row + seg0;
     const bool vec = ((reinterpret_cast<uintptr_t>(row) & 15u) == 0);   // seg0 % 128 == 0
     auto key_at = [&](int o) -> uint32_t { return asp::score_key(__ldg(srow + o)); };
-    // base[o..o+3] (o % 4 == 0), elements >= lim read as 0 (callers mask them).
+    // base[o..o+3] (o % 4 == 0), elements >= lim read as 0.  Callers issue
+    // all their loads before converting any (in-order issue: a conversion
+    // right after its load would serialise the loads).
     auto raw4 = [&](const float *base, int o, int lim) -> float4 {
         if (vec && o + 3 < lim) return __ldg(reinterpret_cast<const float4 *>(base + o));
         float4 v;
@@ -303,10 +260,10 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
         return make_uint4(asp::score_key(v.x), asp::score_key(v.y), asp::score_key(v.z),
                           asp::score_key(v.w));
     };
-    const bool seeded = n <= kRound;         // the classify sweep can seed the bitmaps
-    const int nchunks = (n + 127) >> 7;
+    const bool direct = n <= kRound;         // the classify sweep can seed the bitmaps
 
     zero_hist(s, kBins);
+    for (int i = t; i < kRound / 32; i += kThreads) s.bm_eq[i] = 0;
     if (t == 0) s.n_cand = 0;
     __syncthreads();
 #ifdef ASP_PROFILE_SELECT
@@ -318,7 +275,7 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
     // kept in registers for the second-level histogram
     const int row_chunks = (len + 127) >> 7;
     const int ns = min(kSampleChunks, row_chunks);
-    constexpr int kPerWarp = kSampleChunks / kWarps > 0 ? kSampleChunks / kWarps : 1;
+    constexpr int kPerWarp = kSampleChunks / kWarps;
     uint4 sk[kPerWarp];
     int so[kPerWarp];
     {
@@ -335,12 +292,8 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
 #pragma unroll
     for (int u = 0; u < kPerWarp; u++)
 #pragma unroll
-        for (int c = 0; c < 4; c++) {                  // equal bins aggregated per warp
-            const bool ok = so[u] + c < len;
-            const uint32_t bin = ok ? comp(sk[u], c) >> 20 : 0xFFFFFFFFu;
-            const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-            if (ok && (__ffs(peers) - 1) == lane) atomicAdd(&s.hist[bin], (uint32_t)__popc(peers));
-        }
+        for (int c = 0; c < 4; c++)
+            if (so[u] + c < len) atomicAdd(&s.hist[comp(sk[u], c) >> 20], 1u);
     // sample size: ns full chunks, unless the last one sampled is the row's
     // partial last chunk
     uint32_t m = 128u * ns;
@@ -379,111 +332,94 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
     }
     SPROF(1);
 
-    // ---- 2. classify the segment against the bracket [key_lo, key_hi],
-    // compared in fp32 (v >= lb(K) <=> key(v) >= K, NaN never): per 128-key
-    // chunk, per float4 component c, one ballot for "above the bracket" and
-    // one for "in it".  The above-words seed bm_gt (seeded segments); the
-    // bracketed keys go to the candidate list (warp-aggregated slots).  NaN
-    // detection rides along.
+    // ---- 2. classify the segment: count the keys above the bracket and
+    // collect the bracketed ones (key, offset) into the candidate list; NaN
+    // detection rides along.  A warp step covers 128 consecutive keys, 4 per
+    // lane (one 16-B load).  The bracket is compared in fp32 -- v >= lb(K)
+    // <=> key(v) >= K -- so a key is only formed for the few candidates.
+    // Direct segments (<= kRound keys) only mark both classes in bitmaps
+    // (bm_gt: above, bm_eq: candidate) and gather the candidates afterwards.
+    const int nchunks = (n + 127) >> 7;
     const float f_lo = key_lower_bound(key_lo);
     const float f_above = key_lower_bound((uint64_t)key_hi + 1);
     bool nan = false;
     {
-        uint32_t above = 0;                              // warp-uniform
-        // one 128-key chunk: x[j] = key 32 j + lane (j = 0..3), `rem` keys valid
-        auto chunk = [&](const float (&x)[4], int ch, int rem) {
-            uint32_t ab[4], in[4], nn = 0;
-#pragma unroll
-            for (int j = 0; j < 4; j++) {
-                const bool ok = 32 * j + lane < rem;
-                ab[j] = __ballot_sync(0xffffffffu, ok && x[j] >= f_above);
-                in[j] = __ballot_sync(0xffffffffu, ok && x[j] >= f_lo) & ~ab[j];
-                nn |= ok && x[j] != x[j];
-            }
-            nan |= nn != 0;
-            above += __popc(ab[0]) + __popc(ab[1]) + __popc(ab[2]) + __popc(ab[3]);
-            if (seeded) {                                // above -> bm_gt, bracketed -> bm_eq
-                const uint32_t wa = lane == 0 ? ab[0] : lane == 1 ? ab[1] : lane == 2 ? ab[2] : ab[3];
-                const uint32_t wc = lane == 0 ? in[0] : lane == 1 ? in[1] : lane == 2 ? in[2] : in[3];
-                if (lane < 4) {
-                    s.bm_gt[4 * ch + lane] = wa;
-                    s.bm_eq[4 * ch + lane] = wc;
-                }
-                return;
-            }
-            const uint32_t any = in[0] | in[1] | in[2] | in[3];
-            if (any) {                                   // unseeded (long) segments: warp-uniform
-                const uint32_t lt = (1u << lane) - 1u;
-                const uint32_t tot = __popc(in[0]) + __popc(in[1]) + __popc(in[2]) + __popc(in[3]);
-                uint32_t slot = 0;
-                if (lane == 0) slot = atomicAdd(&s.n_cand, tot);
-                slot = __shfl_sync(0xffffffffu, slot, 0);
-#pragma unroll
-                for (int j = 0; j < 4; j++) {
-                    if ((in[j] >> lane) & 1u) {
-                        const uint32_t sl = slot + __popc(in[j] & lt);
-                        if (sl < (uint32_t)kCand) {
-                            s.cand[sl] = asp::score_key(x[j]);
-                            s.cand_idx[sl] = (uint16_t)(((ch << 7) + 32 * j + lane) & (kRound - 1));
-                        }
-                    }
-                    slot += __popc(in[j]);
-                }
-            }
-        };
+        uint32_t above = 0;
         for (int c0 = warp; c0 < nchunks; c0 += kUnroll * kWarps) {
             const bool full = vec && ((c0 + (kUnroll - 1) * kWarps) << 7) + 128 <= n;
-            float x[kUnroll][4];
+            float4 kv[kUnroll];
             if (full) {
 #pragma unroll
                 for (int u = 0; u < kUnroll; u++)
-#pragma unroll
-                    for (int j = 0; j < 4; j++)
-                        x[u][j] = __ldg(srow + ((c0 + u * kWarps) << 7) + 32 * j + lane);
-#pragma unroll
-                for (int u = 0; u < kUnroll; u++) chunk(x[u], c0 + u * kWarps, 128);
+                    kv[u] = __ldg(reinterpret_cast<const float4 *>(srow + ((c0 + u * kWarps) << 7)) + lane);
             } else {
-#pragma unroll
-                for (int u = 0; u < kUnroll; u++)
-#pragma unroll
-                    for (int j = 0; j < 4; j++) {
-                        const int o = ((c0 + u * kWarps) << 7) + 32 * j + lane;
-                        x[u][j] = o < n ? __ldg(srow + o) : 0.0f;
-                    }
 #pragma unroll
                 for (int u = 0; u < kUnroll; u++) {
                     const int ch = c0 + u * kWarps;
-                    if (ch >= nchunks) break;                      // warp-uniform
-                    chunk(x[u], ch, n - (ch << 7));
+                    kv[u] = raw4(srow, (ch << 7) + 4 * lane, ch < nchunks ? n : 0);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; u++) {
+                const int ch = c0 + u * kWarps;
+                if (ch >= nchunks) break;                      // warp-uniform
+                const int o = (ch << 7) + 4 * lane;
+                const uint32_t valid = full || o + 3 < n ? 0xFu : (0xFu >> min(4, o + 4 - n)) & 0xFu;
+                uint32_t ab = 0, in = 0;
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    const float v = comp(kv[u], c);
+                    nan |= v != v;
+                    ab |= (uint32_t)(v >= f_above) << c;
+                    in |= (uint32_t)(v >= f_lo) << c;
+                }
+                ab &= valid;
+                in &= valid & ~ab;
+                above += __popc(ab);
+                if (direct) {                 // word ch*4 + lane/8 <- nibbles of 8 lanes
+                    uint32_t wa = ab << (4 * (lane & 7)), wc = in << (4 * (lane & 7));
+#pragma unroll
+                    for (int d = 1; d < 8; d <<= 1) {
+                        wa |= __shfl_xor_sync(0xffffffffu, wa, d);
+                        wc |= __shfl_xor_sync(0xffffffffu, wc, d);
+                    }
+                    if ((lane & 7) == 0) {
+                        s.bm_gt[(ch << 2) + (lane >> 3)] = wa;
+                        s.bm_eq[(ch << 2) + (lane >> 3)] = wc;
+                    }
+                } else if (in) {              // order within the list is irrelevant
+                    uint32_t slot = atomicAdd(&s.n_cand, (uint32_t)__popc(in));
+#pragma unroll
+                    for (int c = 0; c < 4; c++) {
+                        if ((in >> c) & 1u) {
+                            if (slot < (uint32_t)kCand) {
+                                s.cand[slot] = asp::score_key(comp(kv[u], c));
+                                s.cand_idx[slot] = (uint32_t)(o + c);
+                            }
+                            slot++;
+                        }
+                    }
                 }
             }
         }
+        above = warp_sum_u32(above);
         const uint32_t a = block_sum_warps(s, above);
-        if (seeded) {
-            // gather the marked candidates (slots from one block scan of the
-            // per-thread counts -- not a shared counter, whose atomics would
-            // serialise) and clear bm_eq
-            const int nw = 4 * nchunks, wpt = (nw + kThreads - 1) / kThreads;
-            const int wa = min(t * wpt, nw), wb = min(wa + wpt, nw);
-            uint32_t cnt = 0;
-            for (int w = wa; w < wb; w++) cnt += __popc(s.bm_eq[w]);
-            uint32_t total;
-            uint32_t slot = block_excl_scan(s, cnt, &total);
-            for (int w = wa; w < wb; w++) {
+        if (direct) {                         // gather the marked candidates; clear bm_eq
+            for (int w = t; w < ((nchunks << 2)); w += kThreads) {
                 uint32_t bits = s.bm_eq[w];
                 if (!bits) continue;
-                s.bm_eq[w] = 0u;
+                s.bm_eq[w] = 0;
+                uint32_t slot = atomicAdd(&s.n_cand, (uint32_t)__popc(bits));
                 while (bits) {
                     const int o = (w << 5) + __ffs(bits) - 1;
                     bits &= bits - 1;
                     if (slot < (uint32_t)kCand) {
                         s.cand[slot] = key_at(o);
-                        s.cand_idx[slot] = (uint16_t)o;
+                        s.cand_idx[slot] = (uint32_t)o;
                     }
                     slot++;
                 }
             }
-            if (t == 0) s.n_cand = total;
         }
         __syncthreads();
         if (t == 0) {
@@ -503,10 +439,8 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
     if (t == 0) atomicAdd(&g_sel_prof[6], (unsigned long long)tot[1]);
 #endif
 
-    // ---- 3. exact T: MSB-first radix select over (key - base), 12 bits per
-    // pass, over the candidates (base = key_lo: the bracket's width bounds the
-    // passes, usually 2) or, when the sample missed, over every key (base 0:
-    // 12 + 12 + 8 bits).  fn(key, candidate slot or -1)
+    // ---- 3. exact T: radix select (12 + 12 + 8 bits) over candidates or all keys
+    // fn(key, candidate slot or -1)
     auto for_each_key = [&](auto &&fn) {
         if (use_cand) {
             const int nc = (int)s.n_cand;
@@ -515,71 +449,40 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
             for (int o = t; o < n; o += kThreads) fn(key_at(o), -1);
         }
     };
-    const uint32_t kbase = use_cand ? key_lo : 0u;
-    const uint64_t width = use_cand ? (uint64_t)key_hi - key_lo + 1 : (1ull << 32);
-    int bits = width <= 1 ? 0 : 64 - __clzll((long long)(width - 1));
-    uint32_t prefix = 0, rank = rank0;
-    while (bits > 0) {
-        const int d = min(12, bits);
-        bits -= d;
-        const int nb = d > 8 ? kBins : 256;
-        zero_hist(s, nb);
-        __syncthreads();
-        const uint64_t pre = prefix;
-        const int sh_hi = bits + d;
-        if (use_cand) {
-            // candidates crowd into a few bins: aggregate equal bins per warp
-            // (one atomic per distinct bin) instead of serialising on them
-            const int nc = (int)s.n_cand;
-            for (int e0 = warp * 32; e0 < nc; e0 += kThreads) {
-                const int e = e0 + lane;
-                const uint64_t rel = e < nc ? (uint64_t)(s.cand[e] - kbase) : 0;
-                const bool hit = e < nc && (rel >> sh_hi) == pre;
-                const uint32_t bin = hit ? (uint32_t)((rel >> bits) & ((1u << d) - 1u)) : 0xFFFFFFFFu;
-                const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-                if (hit && (__ffs(peers) - 1) == lane) atomicAdd(&s.hist[bin], (uint32_t)__popc(peers));
-            }
-        } else {
-            for_each_key([&](uint32_t key, int) {
-                const uint64_t rel = (uint64_t)(key - kbase);
-                if ((rel >> sh_hi) == pre) atomicAdd(&s.hist[(rel >> bits) & ((1u << d) - 1u)], 1u);
-            });
-        }
-        merge_hist(s, nb, C);
-        find_bucket(s, nb, rank, rank);
-        prefix = (prefix << d) | s.found_bin;
-        rank = s.found_rem;
-    }
-    const uint32_t T = kbase + prefix;
-    const uint32_t need = rank;              // keys == T to take, lowest index first
+    zero_hist(s, kBins);
+    __syncthreads();
+    for_each_key([&](uint32_t key, int) { atomicAdd(&s.hist[key >> 20], 1u); });
+    merge_hist(s, kBins, C);
+    find_bucket(s, kBins, rank0, rank0);
+    const uint32_t d1 = s.found_bin, rem1 = s.found_rem;
+    zero_hist(s, kBins);
+    __syncthreads();
+    for_each_key([&](uint32_t key, int) {
+        if ((key >> 20) == d1) atomicAdd(&s.hist[(key >> 8) & 0xFFFu], 1u);
+    });
+    merge_hist(s, kBins, C);
+    find_bucket(s, kBins, rem1, rem1);
+    const uint32_t pre24 = (d1 << 12) | s.found_bin, rem2 = s.found_rem;
+    zero_hist(s, 256);
+    __syncthreads();
+    for_each_key([&](uint32_t key, int) {
+        if ((key >> 8) == pre24) atomicAdd(&s.hist[key & 0xFFu], 1u);
+    });
+    merge_hist(s, 256, C);
+    find_bucket(s, 256, rem2, rem2);
+    const uint32_t T = (pre24 << 8) | s.found_bin;
+    const uint32_t need = s.found_rem;       // keys == T to take, lowest index first
     SPROF(3);
 
-    // ---- 4. this CTA's (key > T, key == T) counts; in a cluster, offsets
-    // after the earlier ranks' keys.  Seeded candidate path: the candidates
-    // that made it join the above-bracket keys in the bitmaps.
-    const bool marked = seeded && use_cand;
-    if (marked) {
-        for_each_key([&](uint32_t key, int e) {
-            const uint32_t o = s.cand_idx[e];
-            if (key > T) atomicOr(&s.bm_gt[o >> 5], 1u << (o & 31u));
-            else if (key == T) atomicOr(&s.bm_eq[o >> 5], 1u << (o & 31u));
-        });
-    }
+    // ---- 4. cluster: this CTA's (key > T, key == T) counts -> offsets after
+    // the earlier ranks' keys
     uint32_t gt_run = 0, eq_run = 0;
     if (C > 1) {
         uint32_t g = 0, e = 0;
-        if (use_cand) {
-            for_each_key([&](uint32_t key, int) {
-                g += key > T;
-                e += key == T;
-            });
-        } else {
-            for (int o = t; o < n; o += kThreads) {
-                const uint32_t key = key_at(o);
-                g += key > T;
-                e += key == T;
-            }
-        }
+        for_each_key([&](uint32_t key, int) {
+            g += key > T;
+            e += key == T;
+        });
         g = block_sum_warps(s, warp_sum_u32(g));
         e = block_sum_warps(s, warp_sum_u32(e));
         if (use_cand) g += cta_above;        // keys above the bracket are all > T
@@ -592,33 +495,87 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
         gt_run = bef2[0];
         eq_run = bef2[1];
     }
-    __syncthreads();
 
-    // ---- 5. emission, one round per kRound keys: bitmaps (seeded, or marked
-    // here by re-reading the keys), chunk offsets, indices in order
+    // ---- 5. emission: bitmaps (key > T, key == T), word offsets, indices in order
+    const bool seeded = direct && use_cand;  // bm_gt holds the keys above the bracket
     for (int r0 = 0; r0 < n; r0 += kRound) {
         const int rn = min(kRound, n - r0);
-        const int rch = (rn + 127) >> 7;
-        if (!marked) {                       // re-read the round's keys: compare with T
-            for (int ch = warp; ch < rch; ch += kWarps) {
-                uint32_t gw = 0, ew = 0;
+        const int rwords = (rn + 31) >> 5;
+        if (seeded) {                        // + the candidates that made it
+            for_each_key([&](uint32_t key, int e) {
+                const uint32_t o = s.cand_idx[e];
+                if (key > T) atomicOr(&s.bm_gt[o >> 5], 1u << (o & 31));
+                else if (key == T) atomicOr(&s.bm_eq[o >> 5], 1u << (o & 31));
+            });
+        } else {
+            const int rchunks = (rn + 127) >> 7;
+            for (int c0 = warp; c0 < rchunks; c0 += 4 * kWarps) {
+                float4 kv[4];
 #pragma unroll
-                for (int j = 0; j < 4; j++) {
-                    const int o = (ch << 7) + 32 * j + lane;
-                    const bool ok = o < rn;
-                    const uint32_t key = ok ? key_at(r0 + o) : 0u;
-                    const uint32_t g = __ballot_sync(0xffffffffu, ok && key > T);
-                    const uint32_t e = __ballot_sync(0xffffffffu, ok && key == T);
-                    if (lane == j) { gw = g; ew = e; }
+                for (int u = 0; u < 4; u++) {
+                    const int ch = c0 + u * kWarps;
+                    kv[u] = raw4(srow + r0, (ch << 7) + 4 * lane, ch < rchunks ? rn : 0);
                 }
-                if (lane < 4) {
-                    s.bm_gt[4 * ch + lane] = gw;
-                    s.bm_eq[4 * ch + lane] = ew;
+                uint4 kk[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) kk[u] = keys4(kv[u]);
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int ch = c0 + u * kWarps;
+                    if (ch >= rchunks) break;                  // warp-uniform
+                    const int o = (ch << 7) + 4 * lane;
+                    uint32_t g = 0, e = 0;
+#pragma unroll
+                    for (int c = 0; c < 4; c++) {
+                        const uint32_t key = comp(kk[u], c);
+                        const bool valid = o + c < rn;
+                        g |= (uint32_t)(valid && key > T) << c;
+                        e |= (uint32_t)(valid && key == T) << c;
+                    }
+                    g <<= 4 * (lane & 7);    // word ch*4 + lane/8 <- nibbles of 8 lanes
+                    e <<= 4 * (lane & 7);
+#pragma unroll
+                    for (int d = 1; d < 8; d <<= 1) {
+                        g |= __shfl_xor_sync(0xffffffffu, g, d);
+                        e |= __shfl_xor_sync(0xffffffffu, e, d);
+                    }
+                    if ((lane & 7) == 0) {
+                        s.bm_gt[(ch << 2) + (lane >> 3)] = g;
+                        s.bm_eq[(ch << 2) + (lane >> 3)] = e;
+                    }
                 }
             }
-            __syncthreads();
         }
-        emit_round(s, 4 * rch, seg0 + r0, need, gt_run, eq_run, out);
+        __syncthreads();
+        const int wpt = (rwords + kThreads - 1) / kThreads;           // words per thread
+        const int wa = min(t * wpt, rwords), wb = min(wa + wpt, rwords);
+        uint32_t cgt = 0, ceq = 0;
+        for (int w = wa; w < wb; w++) {
+            cgt += __popc(s.bm_gt[w]);
+            ceq += __popc(s.bm_eq[w]);
+        }
+        uint32_t tg, te;
+        uint32_t gt_before = gt_run + block_excl_scan(s, cgt, &tg);
+        uint32_t eq_before = eq_run + block_excl_scan(s, ceq, &te);
+        for (int w = wa; w < wb; w++) {
+            const uint32_t g = s.bm_gt[w], e = s.bm_eq[w];
+            uint32_t bits = g | e;
+            while (bits) {
+                const int bit = __ffs(bits) - 1;
+                bits &= bits - 1;
+                const int idx = seg0 + r0 + (w << 5) + bit;
+                if ((g >> bit) & 1u) {
+                    out[gt_before + min(eq_before, need)] = idx;
+                    gt_before++;
+                } else {
+                    if (eq_before < need) out[gt_before + eq_before] = idx;
+                    eq_before++;
+                }
+            }
+        }
+        gt_run += tg;
+        eq_run += te;
+        __syncthreads();                     // the bitmaps are rewritten next round
     }
     nan = __syncthreads_or(nan);
     SPROF(4);
@@ -632,3 +589,4 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
             asm volatile("discard.global.L2 [%0], 128;" ::"l"(x) : "memory");
     }
 }
+

@@ -51,16 +51,50 @@ start = next(i for i, ln in enumerate(lines) if ln.startswith('"ID"'))
 rows = list(csv.reader(lines[start:]))
 h = rows[0]
 keep = [r for r in rows[1:] if any(k in r[h.index("Kernel Name")] for k in
-        ("predict_kernel", "score_tc", "select_kernel", "decode_tc", "decode_combine"))]
+        ("predict_", "score_tc", "select_kernel", "decode_tc", "decode_combine"))]
 with open(os.path.join(dst, f"{tag}_launches.csv"), "w") as f:
     w = csv.writer(f)
     w.writerow(["ID", "Kernel Name", "gpu__time_duration.sum (ns)"])
     for r in keep:
         w.writerow([r[h.index("ID")], r[h.index("Kernel Name")][:90], r[h.index("Metric Value")]])
-    last = keep[-5:]
+    last = keep[-5:]            # predict, score, select, decode, combine of the last step
     tot = sum(float(r[h.index("Metric Value")].replace(",", "")) for r in last)
     f.write("# share of the last step (serialised, cold-cache ncu times):\n")
     for r in last:
         v = float(r[h.index("Metric Value")].replace(",", ""))
         f.write(f"# {r[h.index('Kernel Name')][:40]}: {v/1e3:.1f} us = {100*v/tot:.1f}%\n")
 print(json.dumps(traffic, indent=1))
+
+
+# 4. L2 residency (application replay, --cache-control none)
+l2 = os.path.join(src, f"{tag}_l2.csv")
+if os.path.exists(l2):
+    import collections
+    rows = list(csv.reader(open(l2)))
+    hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    h = rows[hi]
+    d = collections.OrderedDict()
+    for r in rows[hi + 1:]:
+        d.setdefault((int(r[h.index("ID")]), r[h.index("Kernel Name")].split("(")[0].replace("void <unnamed>::", "")),
+                     {})[r[h.index("Metric Name")]] = float(r[h.index("Metric Value")].replace(",", ""))
+    with open(os.path.join(dst, f"{tag}_l2_residency.txt"), "w") as f:
+        f.write("# L2 residency of the score buffer and the decode partials (SURVEY §8(d)), config [2]:\n")
+        f.write("# ncu --replay-mode application --cache-control none --clock-control none (the step's\n")
+        f.write("# kernels as they run back to back: nothing flushes L2 between producer and consumer).\n")
+        f.write("%-4s %-26s %9s %12s %12s %10s %10s %7s\n" % ("id", "kernel", "dur_us", "dram_rd_MB",
+                                                          "dram_wr_MB", "L2rd_MB", "L2hit_MB", "hit%"))
+        for (i, k), m in d.items():
+            rd = m["lts__t_sectors_srcunit_tex_op_read.sum"] * 32 / 1e6
+            hit = m["lts__t_sectors_srcunit_tex_op_read_lookup_hit.sum"] * 32 / 1e6
+            f.write("%-4d %-26s %9.1f %12.2f %12.2f %10.1f %10.1f %7.1f\n" % (
+                i, k[:26], m["gpu__time_duration.sum"] / 1e3, m["dram__bytes_read.sum"] / 1e6,
+                m["dram__bytes_write.sum"] / 1e6, rd, hit, 100 * hit / max(rd, 1e-9)))
+        f.write("# 'lookup miss' sectors that do not reach DRAM are served by the far L2 partition\n")
+
+# 5. the bench lines
+import shutil
+for name in ("bench.json", "bench_reference.json", "bench_ragged.json", "scaling_emulated.jsonl",
+             "bench_paged.jsonl", "bench_variants.jsonl", "launches_p8.csv"):
+    p_src = os.path.join(src, f"{tag}_{name}")
+    if os.path.exists(p_src):
+        shutil.copy(p_src, os.path.join(dst, f"{tag}_{name}"))

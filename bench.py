@@ -385,8 +385,9 @@ def main():
     sh = shard_units(cfg.batch, cfg.n_kv_heads, shards, rank)   # §8(e): KV heads, then batch
     h0, hn = sh.h0, sh.hn
     wdt = torch.bfloat16 if args.bf16_window else torch.float32
+    # multi-GPU: head-major outputs, so the gather below is one concatenation
     step = DecodeStep(cfg, "cuda", kv_heads=(h0, hn), window_dtype=wdt,
-                      batch_range=(sh.b0, sh.bn))
+                      batch_range=(sh.b0, sh.bn), out_head_major=world > 1)
     step.fill_synthetic()
     lens = [cfg.seq_len] * sh.bn
     if args.ragged:
@@ -556,14 +557,16 @@ def main():
     # output all-gather (NCCL) timed separately: in a TP model o_proj consumes the shard
     gather_ms = None
     if world > 1:
-        full = torch.empty(world, *step.out.shape, dtype=step.out.dtype, device="cuda")
+        # head-major shards [Hq/P, B, Dv] -> the global [Hq, B, Dv] by one
+        # all_gather_into_tensor (shard.gather_heads / gather_units)
+        from paper_2510_07486_b200.shard import gather_units
         for _ in range(3):
-            dist.all_gather_into_tensor(full, step.out)
+            full = gather_units(step.out, sh, cfg.batch, cfg.n_q_heads, cfg.group)
         barrier()
         e0, e1 = ev(), ev()
         e0.record(stream)
         for _ in range(10):
-            dist.all_gather_into_tensor(full, step.out)
+            full = gather_units(step.out, sh, cfg.batch, cfg.n_q_heads, cfg.group)
         e1.record(stream)
         barrier()
         gather_ms = e0.elapsed_time(e1) / 10

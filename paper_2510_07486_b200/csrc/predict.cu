@@ -975,7 +975,10 @@ cudaError_t asp_launch_predict(const asp_predict_params &p, const float *q_windo
         (mode == ASP_ASSEMBLY_MASKED_SHARED || mode == ASP_ASSEMBLY_SINGLE)) {
         // few row pairs: slice the head dimension over a CTA's warps (latency);
         // many: two rows per warp (throughput)
-        const bool split = (long)p.batch * p.n_q_heads < 8L * asp_sm_count();
+#ifndef ASP_PREDICT_SPLIT_ROWS_PER_SM
+#define ASP_PREDICT_SPLIT_ROWS_PER_SM 8
+#endif
+        const bool split = (long)p.batch * p.n_q_heads < (long)ASP_PREDICT_SPLIT_ROWS_PER_SM * asp_sm_count();
         if (split) {
             if (p.head_dim == 64) return nb == 1 ? launch_split<64, 1>(p, q_window, q_hat, dev_flags, s)
                                                  : launch_split<64, 2>(p, q_window, q_hat, dev_flags, s);

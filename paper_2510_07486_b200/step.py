@@ -31,7 +31,7 @@ class DecodeStep:
     def __init__(self, cfg: Config, device="cuda", *, kv_heads: tuple[int, int] | None = None,
                  n_fresh: int = 0, eps: float = 1e-2, flags: int = 0, keep_scores: bool = False,
                  layers: int = 1, window_dtype: torch.dtype = torch.float32,
-                 batch_range: tuple[int, int] | None = None):
+                 batch_range: tuple[int, int] | None = None, out_head_major: bool = False):
         self.cfg = cfg
         self.layers = layers
         self.device = torch.device(device)
@@ -58,14 +58,20 @@ class DecodeStep:
         self.seq_lens = torch.full((B,), L, dtype=torch.int32, device=dev)
         self.q_hat = torch.empty(B, self.n_q, D, dtype=torch.float32, device=dev)
         self.sel_idx = torch.empty(B, hn, cfg.top_k, dtype=torch.int32, device=dev)
-        self.out = torch.empty(B, self.n_q, self.dv, dtype=torch.float32, device=dev)
+        # out [B, n_q, Dv], or head-major [n_q, B, Dv]: a KV-head shard's block of
+        # the gathered [Hq, B, Dv] output (the gather is a concatenation)
+        self.out_head_major = out_head_major
+        self.out = (torch.empty(self.n_q, B, self.dv, dtype=torch.float32, device=dev)
+                    if out_head_major else
+                    torch.empty(B, self.n_q, self.dv, dtype=torch.float32, device=dev))
         self.dev_flags = torch.zeros(1, dtype=torch.int32, device=dev)
         self.scores = (torch.empty(B, hn, L, dtype=torch.float32, device=dev)
                        if keep_scores else None)
         self.p_pred = predict_params(self.window, eps, flags, 0)
         self.p_sel = select_params(self.q_hat, self.k_cache, cfg.top_k)
         self.p_dec = decode_params(self.q, self.k_cache, self.v_cache, cfg.top_k, n_fresh,
-                                   v_head_dim=cfg.v_head_dim if self.mla else 0)
+                                   v_head_dim=cfg.v_head_dim if self.mla else 0,
+                                   out_head_major=out_head_major)
         self.ws_sel = torch.empty(max(score_select_workspace(self.p_sel), 256), dtype=torch.uint8,
                                   device=dev)
         self.ws_dec = torch.zeros(max(sparse_decode_workspace(self.p_dec), 256),

@@ -22,7 +22,9 @@ for name, shard in (("qwen3-32b_b64_ctx32k", 1), ("qwen3-32b_b64_ctx32k", 8),
     asp.predict_query(st.window, st.q_hat, params=st.p_pred)
     asp.score_select(st.q_hat, st.k_cache, st.seq_lens, cfg.top_k, sel_idx=st.sel_idx,
                      workspace=st.ws_sel, params=st.p_sel)
-    if os.environ.get("AB_CALL") == "decode":
+    if os.environ.get("AB_CALL") == "predict":
+        f = lambda: asp.predict_query(st.window, st.q_hat, params=st.p_pred)
+    elif os.environ.get("AB_CALL") == "decode":
         f = lambda: asp.sparse_decode(st.q, st.k_cache, st.v_cache, st.seq_lens, st.sel_idx,
                                       out=st.out, workspace=st.ws_dec, params=st.p_dec)
     else:

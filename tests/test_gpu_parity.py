@@ -840,3 +840,24 @@ def test_decode_head_major_out():
         torch.cuda.synchronize()
         assert hm.shape == (cfg.n_q_heads, cfg.batch, cfg.head_dim)
         assert torch.equal(hm.transpose(0, 1), dense)
+
+
+def test_head_major_shards_concatenate_to_the_full_output():
+    """§8(e): with head-major outputs ([Hq/P, B, D] per KV-head shard) the
+    shards' outputs concatenated along the head axis are bit for bit the
+    unsharded run's [B, Hq, D] output transposed -- the all-gather is a plain
+    concatenation (shard.gather_heads)."""
+    cfg = configs.QWEN3_8B.with_(batch=3, seq_len=4096, top_k=256)
+    full = DecodeStep(cfg, DEV, n_fresh=1)
+    full.fill_synthetic()
+    full.run()
+    parts = []
+    for r in range(4):
+        part = DecodeStep(cfg, DEV, kv_heads=(2 * r, 2), n_fresh=1, out_head_major=True)
+        part.fill_synthetic()
+        part.run()
+        parts.append(part.out)
+    torch.cuda.synchronize()
+    cat = torch.cat(parts, dim=0)                     # what all_gather_into_tensor produces
+    assert cat.shape == (cfg.n_q_heads, cfg.batch, cfg.head_dim)
+    assert torch.equal(cat.transpose(0, 1), full.out)

@@ -39,6 +39,13 @@ class AsyncPipeline:
             raise ValueError("the async pipeline decodes with n_fresh = 1 (reading R12)")
         self.step = step
         dev = step.device
+        # the selection is background work: the step's own kernels (push,
+        # decode, forward) run on a HIGH-priority stream, so when both have CTAs
+        # pending the SMs go to the critical path first; the side stream keeps
+        # the default (lowest) priority
+        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") \
+            else (0, -1)
+        self.hi = torch.cuda.Stream(device=dev, priority=hi)
         self.side = torch.cuda.Stream(device=dev)
         self.idx = [step.sel_idx, torch.empty_like(step.sel_idx)]
         self.ev_push = torch.cuda.Event()
@@ -104,16 +111,20 @@ class AsyncPipeline:
         """One decode step t, selection for t+1 overlapped."""
         if not self.primed:
             self.prime()
-        main = torch.cuda.current_stream(self.step.device)
+        caller = torch.cuda.current_stream(self.step.device)
+        main = self.hi
+        main.wait_stream(caller)                  # the step's inputs come from the caller
         cur, nxt = self.t % 2, (self.t + 1) % 2
         main.wait_event(self.ev_sel[cur])
-        self.push(q_t, kv_t)
+        with torch.cuda.stream(main):
+            self.push(q_t, kv_t)
         self.ev_push.record(main)
         self.side.wait_event(self.ev_push)
         self.select(nxt, self.side)
         self.ev_sel[nxt].record(self.side)
         self.decode(cur, main)
         self.forward(main)
+        caller.wait_stream(main)                  # outputs in the caller's order
         self.t += 1
 
     def drain(self) -> None:

@@ -1,6 +1,9 @@
 """A small composed step of every entry point, for compute-sanitizer runs:
 append -> predict -> score_select (dense and paged) -> decode -> gather ->
-quest, on a ragged two-sequence batch; then full steps at G = 16 and G = 32."""
+quest, on a ragged two-sequence batch; then full steps at G = 16 and G = 32,
+the round-2 kernels (head-dim-split predict, G = 64 tensor-core score,
+CUDA-core score / decode for absorbed MLA and 128-head MQA, single-chunk
+direct output, head-major output, window-less append)."""
 import os, sys, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2510_07486_b200 as asp
@@ -31,5 +34,17 @@ for G, hkv in ((16, 2), (32, 1)):
     s2.run()
     flags = int(s2.dev_flags.item())
     assert flags == 0, flags
+# round 2: MQA 64 / 128 heads, absorbed MLA (values from the key rows), a
+# single-chunk decode (k + n_fresh <= 256), head-major output, window-less append
+for c2 in (configs.Config("mqa64", 0, 2, 64, 1, 128, 2048, 256, 16),
+           configs.Config("mqa128", 0, 2, 128, 1, 128, 2048, 128, 16),
+           configs.Config("mla4", 0, 2, 4, 1, 576, 1024, 128, 16, v_head_dim=512)):
+    s2 = DecodeStep(c2, "cuda", n_fresh=1, out_head_major=c2.name == "mqa64")
+    s2.fill_synthetic()
+    s2.run()
+    flags = int(s2.dev_flags.item())
+    assert flags == 0, flags
+q_only = torch.empty(2, 32, 128, dtype=torch.bfloat16, device="cuda")
+asp.append(torch.randn(2, 32, 128, generator=g).cuda(), None, 0, q_cur=q_only)
 torch.cuda.synchronize()
 print("sanitize-small ok, flags", int(st.dev_flags.item()))

@@ -44,6 +44,9 @@ def _args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-a5", action="store_true",
                     help="skip the a5 (asynchronous selection) pipelined measurement")
+    ap.add_argument("--a5-no-forward", action="store_true",
+                    help="a5 without the layer's synthetic forward (the step alone)")
+    ap.add_argument("--a5-priority", default="none", choices=["none", "main", "side"])
     ap.add_argument("--emulate-shard", type=int, default=0, metavar="P",
                     help="one GPU runs rank 0's shard of a P-way KV-head split (the per-GPU "
                          "work of the P-GPU run; scaling evidence when only one GPU is at hand)")
@@ -663,8 +666,8 @@ def main():
         # model's per-layer parameters (Qwen3-32B / Qwen3-8B, Table 1), 1/P per
         # GPU under P-way tensor parallelism
         lp = synth.QWEN3_32B_LAYER_PARAMS if cfg.n_q_heads == 64 else synth.QWEN3_8B_LAYER_PARAMS
-        fwd_bytes = 2 * lp // shards
-        pipe = AsyncPipeline(st1, forward_bytes=fwd_bytes)
+        fwd_bytes = 0 if args.a5_no_forward else 2 * lp // shards
+        pipe = AsyncPipeline(st1, forward_bytes=fwd_bytes, priority=args.a5_priority)
         res = {}
         for _ in range(3):
             pipe.forward(stream)
@@ -695,7 +698,9 @@ def main():
         t_sel = (avg_pred + avg_sel) * 1e3
         a5 = {"serial_us": res["serial"], "pipelined_us": res["pipelined"],
               "forward_us": res["forward"], "forward_bytes": fwd_bytes, "unit": UNIT,
-              "overlap_efficiency": (res["serial"] - res["pipelined"]) / max(min(res["forward"], t_sel), 1e-9),
+              "overlap_efficiency": ((res["serial"] - res["pipelined"]) / max(min(res["forward"], t_sel), 1e-9)
+                                     if fwd_bytes else None),
+              "pipelined_gain_frac": (res["serial"] - res["pipelined"]) / res["serial"],
               "what": "steady-state layer step: selection for t+1 (predict, score, top-k) on a "
                       "side stream overlapped with decode(t) and the layer's synthetic forward "
                       "(weight streaming, %.0f MB) on the main stream; serial = the same calls "

@@ -11,9 +11,12 @@ bool aligned16(const void *ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u
 // the tensor-core kernels (score.cu, decode.cu): head_dim 64 / 128, G <= 32
 bool group_ok(int G) { return G == 1 || G == 2 || G == 4 || G == 8 || G == 16 || G == 32; }
 bool dim_ok(int D) { return D == 64 || D == 128; }
-bool tc_select_ok(const asp_select_params *p) {     // score.cu also runs G = 64 (MQA)
-    const int G = p->n_q_heads / p->n_kv_heads;
-    return dim_ok(p->head_dim) && (group_ok(G) || G == 64);
+bool tc_select_ok(const asp_select_params *p) {     // score.cu's instantiations
+    const int G = p->n_q_heads / p->n_kv_heads, D = p->head_dim;
+    if (dim_ok(D)) return group_ok(G) || G == 64;                 // G = 64: MQA
+    if (D == 576) return G == 1 || G == 2 || G == 4 || G == 8 || G == 16;   // absorbed MLA
+    if (D == 256) return G == 8 || G == 16;
+    return false;
 }
 int v_dim_of(const asp_decode_params *p) { return p->v_head_dim ? p->v_head_dim : p->head_dim; }
 bool tc_decode_ok(const asp_decode_params *p) {
@@ -179,7 +182,7 @@ asp_status asyncspade_score_select_paged(const asp_select_params *p, const asp_p
     q.k_stride_h = q.k_stride_b = 0;
     asp_status st = check_select(&q);
     if (st != ASP_OK) return st;
-    if (!tc_select_ok(&q)) return ASP_ERR_UNSUPPORTED;           // paged: tensor-core shapes
+    if (!tc_select_ok(&q) || !dim_ok(q.head_dim)) return ASP_ERR_UNSUPPORTED;   // paged: D 64 / 128
     st = check_paged(pk, q.n_kv_heads, q.max_seq_len);
     if (st != ASP_OK) return st;
     if (!q_hat || !k_pages || !block_table || !seq_lens || !sel_idx) return ASP_ERR_INVALID_ARGUMENT;

@@ -68,9 +68,22 @@ template <int D, int G>
 struct Cfg {
     static constexpr int N = (3 * G + 15) / 16 * 16 < 16 ? 16 : (3 * G + 15) / 16 * 16;
     static constexpr int kRegions = D / 64;                       // 128-B swizzle rows per token
-    static constexpr int kStageBytes = kTileM * D * 2;
+    // a ring stage holds one 128-token tile (D <= 128), or one 64-dim region of
+    // it for wide keys (absorbed MLA, D = 576: a tile is 9 stages, accumulated
+    // in TMEM across them)
+#ifndef ASP_SCORE_WIDE_REGIONS
+#define ASP_SCORE_WIDE_REGIONS 3
+#endif
+    static constexpr int kRegPerStage = D <= 128 ? kRegions
+                                      : (kRegions % ASP_SCORE_WIDE_REGIONS == 0 ? ASP_SCORE_WIDE_REGIONS
+                                         : (kRegions % 2 == 0 ? 2 : 1));
+    static constexpr int kSub = kRegions / kRegPerStage;          // stages per tile
+    static constexpr int kStageBytes = kTileM * 64 * kRegPerStage * 2;
     static constexpr int kBRegionBytes = N * 128;
     static constexpr int kBSlotBytes = kRegions * kBRegionBytes;
+    // B-operand ring: two slots, one for wide keys (a row's operand is ~55 KB;
+    // MLA has one KV head, so rows change every L / 128 tiles)
+    static constexpr int kBSlots = D <= 128 ? ::kBSlots : 1;
     // accumulation chains per tile: even / odd k-steps in two TMEM halves (short
     // MMAs, latency-bound chains), one chain when N > 96 (G = 64: an N = 192 MMA
     // is long enough, and two halves would leave room for a single stage)
@@ -78,16 +91,17 @@ struct Cfg {
     // accumulator stages: 6, or as many as fit the 512 TMEM columns (G = 16: 5,
     // G = 32: 2, G = 64: 2)
     static constexpr int kAcc = (kHalves * ::kAcc * N) <= 512 ? ::kAcc : 512 / (kHalves * N);
-    // K ring: 6 stages, fewer when the B-operand ring needs the room (G = 32: 5)
-    static constexpr int kStages =
-        (1024 + ::kStages * kTileM * D * 2 + kBSlots * (D / 64) * N * 128 + 256) <= 227 * 1024
-            ? ::kStages
-            : (227 * 1024 - 1024 - kBSlots * (D / 64) * N * 128 - 256) / (kTileM * D * 2);
+    // K ring: 6 tile stages, fewer when the B-operand ring needs the room
+    // (G = 32: 5); wide keys: as many region-group stages as fit, up to 12
+    static constexpr int kFree = 227 * 1024 - 1024 - kBSlots * kBSlotBytes - 512;
+    static constexpr int kStages = D <= 128 ? (kFree / kStageBytes < ::kStages ? kFree / kStageBytes : ::kStages)
+                                            : (kFree / kStageBytes < 12 ? kFree / kStageBytes : 12);
     static constexpr uint32_t kTmemCols = (kHalves * kAcc * N) <= 64 ? 64
                                           : (kHalves * kAcc * N) <= 128 ? 128
                                           : (kHalves * kAcc * N) <= 256 ? 256 : 512;
-    static constexpr int kSmemBytes = 1024 /*align slack*/ + Cfg::kStages * kStageBytes +
-                                      kBSlots * kBSlotBytes + 256 /*barriers*/;
+    static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes +
+                                      kBSlots * kBSlotBytes + 512 /*barriers*/;
+    static_assert(kStages >= 2, "K ring");
 };
 
 // One group of 3 tiles x 8 k-steps (D = 128) in a single asm statement: the
@@ -248,14 +262,14 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
     unsigned char *gbase = smem_raw + (base - raw);
     const uint32_t stage0 = base;
     const uint32_t bslot0 = stage0 + C::kStages * C::kStageBytes;
-    const uint32_t bar0 = bslot0 + kBSlots * C::kBSlotBytes;
+    const uint32_t bar0 = bslot0 + C::kBSlots * C::kBSlotBytes;
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
     auto empty_bar = [&](int s) { return bar0 + 8u * (C::kStages + s); };
     auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * C::kStages + a); };
     auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * C::kStages + C::kAcc + a); };
     auto bfull_bar = [&](int s) { return bar0 + 8u * (2 * C::kStages + 2 * C::kAcc + s); };
-    auto bempty_bar = [&](int s) { return bar0 + 8u * (2 * C::kStages + 2 * C::kAcc + kBSlots + s); };
-    const uint32_t tmem_holder = bar0 + 8u * (2 * C::kStages + 2 * C::kAcc + 2 * kBSlots);
+    auto bempty_bar = [&](int s) { return bar0 + 8u * (2 * C::kStages + 2 * C::kAcc + C::kBSlots + s); };
+    const uint32_t tmem_holder = bar0 + 8u * (2 * C::kStages + 2 * C::kAcc + 2 * C::kBSlots);
     unsigned char *gbslot0 = gbase + (bslot0 - base);
     volatile uint32_t *tmem_holder_g =
         reinterpret_cast<volatile uint32_t *>(gbase + (tmem_holder - base));
@@ -320,7 +334,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::kStages; s++) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
         for (int a = 0; a < C::kAcc; a++) { mbar_init(tfull_bar(a), 1); mbar_init(tempty_bar(a), 4); }
-        for (int s = 0; s < kBSlots; s++) { mbar_init(bfull_bar(s), 1); mbar_init(bempty_bar(s), 1); }
+        for (int s = 0; s < C::kBSlots; s++) { mbar_init(bfull_bar(s), 1); mbar_init(bempty_bar(s), 1); }
         fence_mbar_init();
         prefetch_tmap(&kmap);
     }
@@ -348,14 +362,17 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
                 const int b = row / p.n_kv_heads, h = row % p.n_kv_heads;
                 const int grow = (int)((b * p.k_stride_b + h * p.k_stride_h) / p.k_stride_t) +
                                  j * kTileM;
-                PWAIT(pw_empty, mbar_wait(empty_bar(s), ph ^ 1));
-                mbar_arrive_expect_tx(full_bar(s), C::kStageBytes);
-                const uint32_t dst = stage0 + s * C::kStageBytes;
+#pragma unroll 1
+                for (int sub = 0; sub < C::kSub; sub++) {
+                    PWAIT(pw_empty, mbar_wait(empty_bar(s), ph ^ 1));
+                    mbar_arrive_expect_tx(full_bar(s), C::kStageBytes);
+                    const uint32_t dst = stage0 + s * C::kStageBytes;
 #pragma unroll
-                for (int r = 0; r < C::kRegions; r++)
-                    tma_load_2d(dst + r * (kTileM * 128), &kmap, full_bar(s), r * 64, grow,
-                                kEvictFirst);
-                if (++s == C::kStages) { s = 0; ph ^= 1; }
+                    for (int r = 0; r < C::kRegPerStage; r++)
+                        tma_load_2d(dst + r * (kTileM * 128), &kmap, full_bar(s),
+                                    (sub * C::kRegPerStage + r) * 64, grow, kEvictFirst);
+                    if (++s == C::kStages) { s = 0; ph ^= 1; }
+                }
             }
             PFLUSH(0, pw_empty);
         }
@@ -424,11 +441,52 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
             int cur_row = -1;
             long long pm_full = 0, pm_tempty = 0, pm_issue = 0, pm_b = 0;
             long i = it.next(it.start);
+            if constexpr (C::kSub > 1) {
+                // wide keys: a tile is kSub region stages accumulated in one TMEM
+                // stage (two chains: even / odd k-steps), tile after tile
+                while (i < it.end) {
+                    const int row = it.row;
+                    if (row != cur_row) {
+                        if (bs >= 0) mma_commit_warp(bempty_bar(bs));
+                        bs = (bs + 1) % C::kBSlots;
+                        if (bs == 0 && cur_row != -1) bph ^= 1;
+                        mbar_wait(bfull_bar(bs), bph);
+                        cur_row = row;
+                    }
+                    mbar_wait(tempty_bar(a), aph ^ 1);
+                    const uint32_t dcol = tmem_base + a * (C::kHalves * N);
+                    const uint64_t bdesc0 = desc_sw128_kmajor(bslot0 + bs * C::kBSlotBytes);
+#pragma unroll 1
+                    for (int sub = 0; sub < C::kSub; sub++) {
+                        mbar_wait(full_bar(s), ph);
+                        tc_fence_after();
+                        const uint64_t adesc = desc_sw128_kmajor(stage0 + s * C::kStageBytes);
+#pragma unroll
+                        for (int kk = 0; kk < 4 * C::kRegPerStage; kk++) {
+                            const int r = kk / 4, ko = (kk % 4) * 32;
+                            const int kg = sub * 4 * C::kRegPerStage + kk;   // k-step in the tile
+                            const uint64_t aoff = (uint64_t)((r * (kTileM * 128) + ko) >> 4);
+                            const uint64_t boff = (uint64_t)(((sub * C::kRegPerStage + r) *
+                                                              C::kBRegionBytes + ko) >> 4);
+                            if constexpr (C::kHalves == 2)
+                                mma_bf16_warp(dcol + (kg & 1) * N, adesc + aoff, bdesc0 + boff, idesc,
+                                              kg > 1 ? 1u : 0u);
+                            else
+                                mma_bf16_warp(dcol, adesc + aoff, bdesc0 + boff, idesc, kg > 0 ? 1u : 0u);
+                        }
+                        mma_commit_warp(empty_bar(s));
+                        if (++s == C::kStages) { s = 0; ph ^= 1; }
+                    }
+                    mma_commit_warp(tfull_bar(a));
+                    if (++a == C::kAcc) { a = 0; aph ^= 1; }
+                    i = it.next(i + 1);
+                }
+            } else
             while (i < it.end) {
                 const int row = it.row;
                 if (row != cur_row) {
                     if (bs >= 0) mma_commit_warp(bempty_bar(bs));   // previous row's B slot free
-                    bs = (bs + 1) % kBSlots;
+                    bs = (bs + 1) % C::kBSlots;
                     if (bs == 0 && cur_row != -1) bph ^= 1;
                     PWAIT(pm_b, mbar_wait(bfull_bar(bs), bph));
                     cur_row = row;
@@ -507,7 +565,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
             const int row = it.row;
             if (row == cur_row) continue;
             cur_row = row;
-            bs = (bs + 1) % kBSlots;
+            bs = (bs + 1) % C::kBSlots;
             if (bs == 0 && i != it.next(it.start)) bph ^= 1;
             mbar_wait(bempty_bar(bs), bph ^ 1);
             const int b = row / p.n_kv_heads, h = row % p.n_kv_heads;
@@ -735,6 +793,9 @@ cudaError_t asp_launch_score(const asp_select_params &p, const float *q_hat,
     ASP_CASE(128, 1) ASP_CASE(128, 2) ASP_CASE(128, 4) ASP_CASE(128, 8)
     ASP_CASE(64, 16) ASP_CASE(128, 16) ASP_CASE(64, 32) ASP_CASE(128, 32)
     ASP_CASE(64, 64) ASP_CASE(128, 64)
+    // absorbed MLA (576-dim latent + rope keys) and 256-dim heads: region stages
+    ASP_CASE(576, 1) ASP_CASE(576, 2) ASP_CASE(576, 4) ASP_CASE(576, 8) ASP_CASE(576, 16)
+    ASP_CASE(256, 8) ASP_CASE(256, 16)
 #undef ASP_CASE
     return cudaErrorInvalidValue;
 }

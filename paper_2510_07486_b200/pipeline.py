@@ -34,19 +34,19 @@ from .step import DecodeStep
 
 
 class AsyncPipeline:
-    def __init__(self, step: DecodeStep, forward_bytes: int = 0):
+    def __init__(self, step: DecodeStep, forward_bytes: int = 0, priority: str = "none"):
         if step.n_fresh != 1:
             raise ValueError("the async pipeline decodes with n_fresh = 1 (reading R12)")
         self.step = step
         dev = step.device
-        # the selection is background work: the step's own kernels (push,
-        # decode, forward) run on a HIGH-priority stream, so when both have CTAs
-        # pending the SMs go to the critical path first; the side stream keeps
-        # the default (lowest) priority
-        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") \
-            else (0, -1)
-        self.hi = torch.cuda.Stream(device=dev, priority=hi)
-        self.side = torch.cuda.Stream(device=dev)
+        # stream priorities (CTA scheduling order when both streams have work
+        # pending): "none" (default, measured best overall), "main" (the step's
+        # push / decode / forward first) or "side" (the selection chain first)
+        if priority not in ("none", "main", "side"):
+            raise ValueError("priority: none, main or side")
+        top = torch.cuda.Stream.priority_range()[1] if priority != "none" else 0
+        self.hi = (torch.cuda.Stream(device=dev, priority=top) if priority == "main" else None)
+        self.side = torch.cuda.Stream(device=dev, priority=top if priority == "side" else 0)
         self.idx = [step.sel_idx, torch.empty_like(step.sel_idx)]
         self.ev_push = torch.cuda.Event()
         self.ev_sel = [torch.cuda.Event(), torch.cuda.Event()]
@@ -112,8 +112,9 @@ class AsyncPipeline:
         if not self.primed:
             self.prime()
         caller = torch.cuda.current_stream(self.step.device)
-        main = self.hi
-        main.wait_stream(caller)                  # the step's inputs come from the caller
+        main = self.hi if self.hi is not None else caller
+        if main is not caller:
+            main.wait_stream(caller)              # the step's inputs come from the caller
         cur, nxt = self.t % 2, (self.t + 1) % 2
         main.wait_event(self.ev_sel[cur])
         with torch.cuda.stream(main):
@@ -124,7 +125,8 @@ class AsyncPipeline:
         self.ev_sel[nxt].record(self.side)
         self.decode(cur, main)
         self.forward(main)
-        caller.wait_stream(main)                  # outputs in the caller's order
+        if main is not caller:
+            caller.wait_stream(main)              # outputs in the caller's order
         self.t += 1
 
     def drain(self) -> None:

@@ -37,6 +37,20 @@
  *   the optional device word `dev_flags` and produce the defined fallback
  *   output documented per call.
  *
+ * Stream ordering (programmatic dependent launch)
+ *   Every kernel is launched with programmatic stream serialization, so its
+ *   prologue overlaps the previous kernel's tail.  Reads of inputs that only
+ *   the CALLER (or asyncspade_append) writes may start before the previous
+ *   kernel on the stream has finished: predict reads the window, the score
+ *   stream reads K, and the score planning reads seq_lens early.  This is
+ *   safe because asyncspade_append never lets its dependents start before it
+ *   completes, and a kernel that does not trigger dependents early (any
+ *   torch / cuBLAS / caller kernel) runs to completion before the next one
+ *   starts; a caller kernel that issues griddepcontrol.launch_dependents
+ *   before writing these buffers must not directly precede these calls.
+ *   Everything else (q_hat, selections, outputs, workspaces) is touched only
+ *   after the wait.
+ *
  * Determinism
  *   Every output row is a function of that row's inputs and the call's
  *   sizes only -- never of the grid, the SM count, the batch size or how

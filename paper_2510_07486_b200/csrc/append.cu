@@ -20,8 +20,10 @@ append_kernel(asp_append_params p, const float *__restrict__ q_t, float *__restr
     const int D = p.head_dim, W = p.window;
     // every write below overwrites state an earlier kernel of the step reads
     // (the window slot, the current query, the cache row): wait for them
+    // No early trigger: the kernels after append (predict, score) read the window
+    // and K before their own programmatic-dependent-launch wait, which is safe
+    // only because they cannot start before append has completed.
     asp::pdl_wait();
-    asp::pdl_trigger();
     const int nq4 = p.n_q_heads * D / 4;
     for (int i = t; i < nq4; i += kThreads) {
         const int hq = (4 * i) / D, d = (4 * i) % D;

@@ -596,7 +596,11 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long rows = (long)p.batch * p.n_q_heads;
     const long row0 = ((long)blockIdx.x * (blockDim.x >> 5) + warp) * 2;
-    asp::pdl_wait();                 // the window may come from asyncspade_append
+    // The window is read before the programmatic-dependent-launch wait: its only
+    // writer in the library, asyncspade_append, does not trigger its dependents
+    // early, so a kernel after it starts only once it has completed (and a
+    // caller's own kernels never trigger early).  q_hat / the flags are written
+    // after the wait (the previous step's kernels may still run).
     asp::pdl_trigger();
     if (row0 >= rows) return;
     const bool has1 = row0 + 1 < rows;
@@ -752,6 +756,7 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
     for (int u = 0; u < kV; u++)
 #pragma unroll
         for (int z = 0; z < 4; z++) acc[u][z] += acc2[u][z];
+    asp::pdl_wait();
     if (live && ok) {
         const double inv_m = 1.0 / denom;
 #pragma unroll
@@ -792,8 +797,7 @@ predict_split_kernel(asp_predict_params p, const float *__restrict__ q_window,
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long rows = (long)p.batch * p.n_q_heads;
     const long row0 = (long)blockIdx.x * 2;
-    asp::pdl_wait();                 // the window may come from asyncspade_append
-    asp::pdl_trigger();
+    asp::pdl_trigger();              // window read before the wait: see predict_pair_kernel
     const bool has1 = row0 + 1 < rows;
     const int rs = p.ring_start;
     auto phys_of = [&](int i) {
@@ -878,6 +882,7 @@ predict_split_kernel(asp_predict_params p, const float *__restrict__ q_window,
         }
     }
     __syncthreads();
+    asp::pdl_wait();                 // q_hat / flags written from here on
     // ---- q_hat slice = (1/m) sum_p c_p Q[p]: each lane weights its two rows,
     // the 8 lanes of a column (same fc) reduce by shuffle
 #pragma unroll

@@ -345,7 +345,12 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
     const uint32_t tmem_base = *tmem_holder_g;
     it.start = s_rng[0];
     it.end = s_rng[1];
-    asp::pdl_wait();                        // q_hat, K (asyncspade_append writes it), scores
+    // The TMA warp streams K before the programmatic-dependent-launch wait (K's
+    // only writer in the library, asyncspade_append, does not trigger early, so
+    // this kernel starts after it completed): the first tiles land while the
+    // previous kernel (predict) finishes.  Everything that reads q_hat or writes
+    // the scores waits.
+    if (warp != 0 || PAGED) asp::pdl_wait();   // (the paged producer reads the block table)
     asp::pdl_trigger();
 #ifdef ASP_PROFILE_SCORE
     const long long t_kernel0 = clock64();

@@ -23,7 +23,8 @@ SYNTH_LIB = os.path.join(PKG, "libasp_synth.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v",
               "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC]
-PRODUCT_SOURCES = ["abi.cu", "append.cu", "predict.cu", "score.cu", "select.cu", "decode.cu",
+PRODUCT_SOURCES = ["abi.cu", "append.cu", "predict.cu", "score.cu", "select.cu", "select_short.cu",
+                   "decode.cu",
                    "score_cc.cu", "decode_cc.cu",
                    "quest.cu", "gather.cu"]
 SYNTH_SOURCES = ["synth.cu"]

@@ -84,10 +84,21 @@ long ceil_div(long a, long b) { return (a + b - 1) / b; }
 
 }  // namespace
 
+cudaError_t asp_launch_select_short(const asp_select_params &p, const float *scores,
+                                    const int32_t *seq_lens, int32_t *sel_idx, uint32_t *dev_flags,
+                                    bool discard_scores, cudaStream_t s);
+
 cudaError_t asp_launch_select(const asp_select_params &p, const float *scores,
                               const int32_t *seq_lens, int32_t *sel_idx, uint32_t *dev_flags,
                               bool discard_scores, cudaStream_t s) {
     const long L = p.max_seq_len;
+#ifndef ASP_SELECT_SHORT_MAX
+#define ASP_SELECT_SHORT_MAX 4096
+#endif
+    // short rows (<= 4k keys): the whole row in one CTA's registers, exact radix
+    // select with no sample / candidate phases (select_short.cu)
+    if (L <= ASP_SELECT_SHORT_MAX)
+        return asp_launch_select_short(p, scores, seq_lens, sel_idx, dev_flags, discard_scores, s);
     const long rows = (long)p.batch * p.n_kv_heads;
     // Cluster size (measured on B200): segments of <= 64k keys, then split
     // further only while the rows could not even occupy a quarter of the SMs,

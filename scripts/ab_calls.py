@@ -14,8 +14,9 @@ import paper_2510_07486_b200 as asp
 from paper_2510_07486_b200 import configs
 from paper_2510_07486_b200.step import DecodeStep
 res = []
-for name, shard in (("qwen3-32b_b64_ctx32k", 1), ("qwen3-32b_b64_ctx32k", 8),
-                    ("high-conc_b512_ctx4k", 1), ("long-cot_b8_ctx524288", 8)):
+WL = os.environ.get("AB_WORKLOADS", "qwen3-32b_b64_ctx32k:1,qwen3-32b_b64_ctx32k:8,"
+                    "high-conc_b512_ctx4k:1,long-cot_b8_ctx524288:8")
+for name, shard in ((w.split(":")[0], int(w.split(":")[1])) for w in WL.split(",")):
     cfg = configs.by_name(name)
     st = DecodeStep(cfg, "cuda", kv_heads=(0, cfg.n_kv_heads // shard))
     st.fill_synthetic()
@@ -35,7 +36,7 @@ for name, shard in (("qwen3-32b_b64_ctx32k", 1), ("qwen3-32b_b64_ctx32k", 8),
     e0.record()
     for _ in range(20): f()
     e1.record(); torch.cuda.synchronize()
-    res.append("%%s/P%%d %%.1f" %% (name.split("_")[0], shard, e0.elapsed_time(e1) / 20 * 1e3))
+    res.append("%%s/P%%d %%.1f" %% (name, shard, e0.elapsed_time(e1) / 20 * 1e3))
     del st; torch.cuda.empty_cache()
 print(" | ".join(res))
 ''' % ROOT

@@ -1,6 +1,7 @@
 // select_short.cu -- a3 (per-row top-k, ties to the lower index, ascending
 // output; P:191, P:267 item (2); readings R9, R13, R14) for SHORT rows
-// (<= 8192 tokens: config [4]'s 4k-token rows, the short end of config [3]).
+// (<= 4096 tokens, the cut in select.cu: config [4]'s 4k-token rows, the
+// short end of config [3]; 8k rows measured slower here than the general kernel).
 //
 // Many short rows (4096 rows of 4096 keys at config [4] batch 512) make the
 // general select kernel latency-bound: its sample -> bracket -> classify ->
@@ -172,7 +173,7 @@ select_short_kernel(asp_select_params p, const float *__restrict__ scores,
 
 }  // namespace
 
-// rows of at most 8192 keys (the caller checks max_seq_len)
+// rows of at most 8192 keys (KPT 16 or 32; select.cu routes only <= 4096 here)
 cudaError_t asp_launch_select_short(const asp_select_params &p, const float *scores,
                                     const int32_t *seq_lens, int32_t *sel_idx, uint32_t *dev_flags,
                                     bool discard_scores, cudaStream_t s) {

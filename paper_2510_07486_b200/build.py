@@ -80,10 +80,14 @@ def build(verbose: bool = False) -> list[str]:
     return [LIB, SYNTH_LIB]
 
 
-def build_profiling(defines: list[str]) -> str:
-    """Instrumented variant (e.g. -DASP_PROFILE_SCORE) at build/prof/ -- dev only."""
-    out_dir = os.path.join(BUILD, "prof")
+def build_profiling(defines: list[str], tag: str = "prof") -> str:
+    """Instrumented variant (e.g. -DASP_PROFILE_SCORE) at build/<tag>/ -- dev only."""
+    out_dir = os.path.join(BUILD, tag)
     os.makedirs(out_dir, exist_ok=True)
+    out = os.path.join(out_dir, "libasyncspade_prof.so")
+    srcs = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    if os.path.exists(out) and os.path.getmtime(out) > max(os.path.getmtime(f) for f in srcs):
+        return out                                   # prebuilt (e.g. here, before a gpurun call)
     objs = []
     for f in PRODUCT_SOURCES:
         obj = os.path.join(out_dir, f + ".o")

@@ -19,7 +19,7 @@
 //   * Persistent CTAs (one per SM) own a contiguous range of the VALID
 //     128-token tiles of the flattened (row, tile) space (balanced over the
 //     rows' actual lengths, so ragged batches keep every SM busy).  Paged
-//     pools stream page-sized TMA boxes, page ids fetched three tiles ahead.
+//     pools stream page-sized TMA boxes, page ids fetched six tiles ahead.
 //     Warp roles: warp 0 streams K tiles
 //     with TMA (4-D tensor map over the strided cache, 128-B swizzle,
 //     L2 evict-first) into a 6-stage mbarrier ring; warp 1 owns TMEM and
@@ -58,7 +58,10 @@ namespace {
 using namespace asp::tc;
 
 constexpr int kTileM = 128;           // tokens per tile (MMA M)
-constexpr int kStages = 6;            // K-tile ring depth
+#ifndef ASP_SCORE_STAGES
+#define ASP_SCORE_STAGES 6
+#endif
+constexpr int kStages = ASP_SCORE_STAGES;   // K-tile ring depth
 constexpr int kAcc = 6;               // TMEM accumulator stages
 constexpr int kGroup = 3;             // tiles whose MMA chains are interleaved
 constexpr int kBSlots = 2;            // B-operand ring
@@ -391,32 +394,33 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
         // warp walks the tile sequence: lanes < NP fetch the page ids of the
         // tile kAhead positions ahead (one block-table word each), so the
         // lookups never stall the stream, and issue that page's copies.
-        constexpr int kAhead = 3;
+        constexpr int kAhead = 6;
         const int P = pg.page_size, NP = kTileM / pg.page_size;
         TileIter ahead = it;
         long ia = ahead.next(it.start);
+        // (the id is clamped where it is used, not here: the load stays in
+        // flight for kAhead tiles instead of stalling the warp right away)
         auto fetch = [&]() -> int {
             int id = 0;
             if (ia < it.end) {
                 const int row = ahead.row, b = row / p.n_kv_heads;
                 const int lp = ahead.j * NP + lane;
-                if (lane < NP && lp * P < ahead.len_of(row)) {
+                if (lane < NP && lp * P < ahead.len_of(row))
                     id = __ldg(pg.block_table + (size_t)b * pg.max_pages + lp);
-                    id = min(max(id, 0), pg.num_pages - 1);     // never fault on a bad entry
-                }
                 ia = ahead.next(ia + 1);
             }
             return id;
         };
-        int q0 = fetch(), q1 = fetch(), q2 = fetch();
-        static_assert(kAhead == 3, "the page-id queue is q0..q2");
+        int q[kAhead];
+#pragma unroll
+        for (int u = 0; u < kAhead; u++) q[u] = fetch();
         int s = 0;
         uint32_t ph = 0;
         for (long i = it.next(it.start); i < it.end; i = it.next(i + 1)) {
-            const int cur = q0;
-            q0 = q1;
-            q1 = q2;
-            q2 = fetch();
+            const int cur = min(max(q[0], 0), pg.num_pages - 1);   // never fault on a bad entry
+#pragma unroll
+            for (int u = 0; u + 1 < kAhead; u++) q[u] = q[u + 1];
+            q[kAhead - 1] = fetch();
             const int h = it.row % p.n_kv_heads;
             mbar_wait(empty_bar(s), ph ^ 1);
             if (lane == 0) mbar_arrive_expect_tx(full_bar(s), C::kStageBytes);

@@ -135,3 +135,12 @@ cudaError_t asp_launch_select(const asp_select_params &p, const float *scores,
     ASP_SELECT_LAUNCH(sel256);
 #undef ASP_SELECT_LAUNCH
 }
+
+#ifdef ASP_PROFILE_SELECT
+// dev only (instrumented build): the select kernel alone on a caller-kept score buffer
+extern "C" __attribute__((visibility("default"))) int asp_select_only(
+    const asp_select_params *p, const float *scores, const int32_t *seq_lens, int32_t *sel_idx,
+    uint32_t *dev_flags, void *stream) {
+    return (int)asp_launch_select(*p, scores, seq_lens, sel_idx, dev_flags, false, (cudaStream_t)stream);
+}
+#endif

@@ -5,7 +5,10 @@ import ctypes, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2510_07486_b200 import build as asp_build
-os.environ["ASYNCSPADE_LIB"] = asp_build.build_profiling(["-DASP_PROFILE_SELECT"])
+_extra = os.environ.get("SEL_DEFINES", "").split()
+os.environ["ASYNCSPADE_LIB"] = asp_build.build_profiling(["-DASP_PROFILE_SELECT", *_extra],
+                                                         tag="prof" + "".join(d.replace("-D", "_") for d in _extra))
+print("select defines:", _extra or "(default)")
 import torch
 import paper_2510_07486_b200 as asp
 from paper_2510_07486_b200 import configs
@@ -25,7 +28,7 @@ for P in [int(x) for x in os.environ.get("SHARDS", "1,8").split(",")]:
         f()
         torch.cuda.synchronize()
     L.asp_select_prof_read(buf)
-    names = ["sample", "bracket", "classify", "radix", "emit"]
+    names = ["sample", "bracket", "gather", "radix", "emit", "sweep"]
     rows = cfg.batch * cfg.n_kv_heads // P
     mhz = 1.965e3
     print(f"{cfg.name} P={P}: {rows} rows")
@@ -39,5 +42,24 @@ for P in [int(x) for x in os.environ.get("SHARDS", "1,8").split(",")]:
     e1.record()
     torch.cuda.synchronize()
     print(f"  score_select call {e0.elapsed_time(e1) / 10 * 1e3:.1f} us (instrumented build)")
-    del step
+    # the select kernel alone, on a kept score buffer (scores L2-warm after the first call)
+    sc = torch.empty(step.sel_idx.shape[0], step.sel_idx.shape[1], cfg.seq_len, dtype=torch.float32, device="cuda")
+    asp.score_select(step.q_hat, step.k_cache, step.seq_lens, cfg.top_k, sel_idx=step.sel_idx,
+                     scores=sc, workspace=step.ws_sel, params=step.p_sel)
+    ref_idx = step.sel_idx.clone()
+    so = lambda: L.asp_select_only(ctypes.byref(step.p_sel), ctypes.c_void_p(sc.data_ptr()),
+                                   ctypes.c_void_p(step.seq_lens.data_ptr()),
+                                   ctypes.c_void_p(step.sel_idx.data_ptr()), None,
+                                   ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    for _ in range(3):
+        so()
+    torch.cuda.synchronize()
+    assert torch.equal(step.sel_idx, ref_idx), "select-only differs from score_select"
+    e0.record()
+    for _ in range(20):
+        so()
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"  select alone {e0.elapsed_time(e1) / 20 * 1e3:.1f} us per call (20 back-to-back calls)")
+    del step, sc
     torch.cuda.empty_cache()

@@ -592,17 +592,17 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
 #endif
 }
 
+// Few chunks (<= kCombineShort, e.g. config [2]'s 9): one sequential pass
+// per thread, the loads of 8 chunks in flight -- no barriers.
+constexpr int kCombineShort = 16;
 template <int D>
 __global__ void __launch_bounds__(D)
-decode_combine_kernel(asp_decode_params p, const float *__restrict__ partials,
-                      float *__restrict__ out, int n_splits) {
+decode_combine_short_kernel(asp_decode_params p, const float *__restrict__ partials,
+                            float *__restrict__ out, int n_splits) {
     const int hq = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
     asp::pdl_wait();
     asp::pdl_trigger();
     const float *src = partials + ((size_t)b * p.n_q_heads + hq) * n_splits * (D + 2);
-    // chunk order is the merge order; unrolled by 8 so the loads of 8 chunks
-    // are in flight together (long-CoT rows have 128 chunks: one dependent L2
-    // round trip each would dominate), the arithmetic stays sequential in s
     float M = -INFINITY;
 #pragma unroll 8
     for (int s = 0; s < n_splits; s++) M = fmaxf(M, src[(size_t)s * (D + 2)]);
@@ -614,6 +614,61 @@ decode_combine_kernel(asp_decode_params p, const float *__restrict__ partials,
             const float a = exp2f(ps[0] - M);
             L = fmaf(ps[1], a, L);
             O = fmaf(ps[2 + d], a, O);
+        }
+    }
+    const int64_t osb = p.out_stride_b ? p.out_stride_b : (int64_t)p.n_q_heads * D;
+    const int64_t osh = p.out_stride_h ? p.out_stride_h : (int64_t)D;
+    out[b * osb + hq * osh + d] = (L > 0.0f) ? O / L : 0.0f;
+    __syncthreads();
+    const uintptr_t lo = (reinterpret_cast<uintptr_t>(src) + 127u) & ~(uintptr_t)127u;
+    const uintptr_t hi = reinterpret_cast<uintptr_t>(src + (size_t)n_splits * (D + 2));
+    for (uintptr_t x = lo + (uintptr_t)d * 128u; x + 128u <= hi; x += (uintptr_t)D * 128u)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(x) : "memory");
+}
+
+// Many chunks (long-CoT rows: 128): the chunk scales are computed once, in
+// parallel, and staged in shared memory; the merge keeps the same order and
+// the same fma chains (bit-identical to the short kernel), with only the
+// partial-output loads on each thread's critical path.
+template <int D>
+__global__ void __launch_bounds__(D)
+decode_combine_kernel(asp_decode_params p, const float *__restrict__ partials,
+                      float *__restrict__ out, int n_splits) {
+    extern __shared__ float s_comb[];           // [n_splits] scales a_s, [n_splits] l_s
+    __shared__ float s_wmax[D / 32];
+    const int hq = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
+    asp::pdl_wait();
+    asp::pdl_trigger();
+    const float *src = partials + ((size_t)b * p.n_q_heads + hq) * n_splits * (D + 2);
+    // 1. every chunk's (m_s, l_s) once, thread s of each block of D chunks
+    //    (one round trip for up to D chunks), the row max by a block reduction
+    float M = -INFINITY;
+    for (int s = d; s < n_splits; s += D) {
+        const float m = src[(size_t)s * (D + 2)];
+        s_comb[s] = m;
+        s_comb[n_splits + s] = src[(size_t)s * (D + 2) + 1];
+        M = fmaxf(M, m);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    if ((d & 31) == 0) s_wmax[d >> 5] = M;
+    __syncthreads();
+    M = s_wmax[0];
+#pragma unroll
+    for (int w = 1; w < D / 32; w++) M = fmaxf(M, s_wmax[w]);
+    // 2. the scale of each chunk, a_s = 2^(m_s - M), computed once
+    if (M != -INFINITY)
+        for (int s = d; s < n_splits; s += D) s_comb[s] = exp2f(s_comb[s] - M);
+    __syncthreads();
+    // 3. the merge in chunk order (the same sequential fma chains as ever); the
+    //    partial-output loads are independent of the chain: 16 in flight
+    float L = 0.0f, O = 0.0f;
+    if (M != -INFINITY) {
+#pragma unroll 16
+        for (int s = 0; s < n_splits; s++) {
+            const float a = s_comb[s];
+            L = fmaf(s_comb[n_splits + s], a, L);
+            O = fmaf(src[(size_t)s * (D + 2) + 2 + d], a, O);
         }
     }
     const int64_t osb = p.out_stride_b ? p.out_stride_b : (int64_t)p.n_q_heads * D;
@@ -651,7 +706,15 @@ cudaError_t launch(const asp_decode_params &p, const asp_bf16 *q, const asp_bf16
     e = asp_launch(kern, dim3(grid), dim3(kThreads), C::kSmemBytes, s, 1, p, q, k, v, seq_lens,
                    idx, partials, out, ns, pg);
     if (e != cudaSuccess || ns == 1) return e;            // one chunk: written directly
-    return asp_launch(decode_combine_kernel<D>, dim3(p.n_q_heads, p.batch), dim3(D), 0, s, 1, p,
+    if (ns <= kCombineShort)
+        return asp_launch(decode_combine_short_kernel<D>, dim3(p.n_q_heads, p.batch), dim3(D), 0, s, 1,
+                          p, (const float *)partials, out, ns);
+    const int csmem = (int)(2 * ns * sizeof(float));     // chunk scales + sums (top_k < ~7M)
+    if (csmem > 48 * 1024) {
+        e = cudaFuncSetAttribute(decode_combine_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem);
+        if (e != cudaSuccess) return e;
+    }
+    return asp_launch(decode_combine_kernel<D>, dim3(p.n_q_heads, p.batch), dim3(D), csmem, s, 1, p,
                       (const float *)partials, out, ns);
 }
 

@@ -63,18 +63,32 @@ extern "C" __attribute__((visibility("default"))) int asp_select_prof_read(unsig
 namespace sel256 {
 #define SEL_NT 256
 #define SEL_MINB 4
+#define SEL_ROUND 32768
 #include "select_impl.cuh"
 #undef SEL_NT
 #undef SEL_MINB
+#undef SEL_ROUND
 }  // namespace sel256
 
 namespace sel1024 {
 #define SEL_NT 1024
 #define SEL_MINB 1
+#define SEL_ROUND 32768
 #include "select_impl.cuh"
 #undef SEL_NT
 #undef SEL_MINB
+#undef SEL_ROUND
 }  // namespace sel1024
+
+namespace sel1024w {              // 64k-key segments (long rows over a cluster)
+#define SEL_NT 1024
+#define SEL_MINB 1
+#define SEL_ROUND 65536
+#include "select_impl.cuh"
+#undef SEL_NT
+#undef SEL_MINB
+#undef SEL_ROUND
+}  // namespace sel1024w
 
 namespace {
 
@@ -131,6 +145,7 @@ cudaError_t asp_launch_select(const asp_select_params &p, const float *scores,
                           dim3(NS::kThreads), smem, s, (unsigned)C, p, scores, seq_lens,   \
                           sel_idx, dev_flags, C, seg, discard_scores ? 1 : 0);             \
     } while (0)
+    if (wide && seg > 32768) ASP_SELECT_LAUNCH(sel1024w);
     if (wide) ASP_SELECT_LAUNCH(sel1024);
     ASP_SELECT_LAUNCH(sel256);
 #undef ASP_SELECT_LAUNCH

@@ -6,7 +6,11 @@ constexpr int kThreads = SEL_NT;
 constexpr int kWarps = kThreads / 32;
 constexpr int kBins = 4096;
 constexpr int kCand = 2048;                   // candidate slots per CTA
-constexpr int kRound = 32768;                 // keys per emission round (bitmap size)
+// keys per emission round (bitmap size): a segment of up to kRound keys is
+// "direct" -- its classify sweep seeds the emission bitmaps, so the keys are
+// read once.  32k, or 64k for the 64k-key segments of rows split over a
+// cluster (1024-thread CTAs, one per SM, afford the bitmaps).
+constexpr int kRound = SEL_ROUND;
 constexpr int kSampleChunks = 32;             // 32 x 128 consecutive keys sampled per row
 constexpr int kMaxCluster = 16;
 constexpr int kUnroll = 8;                    // 16-B loads in flight per lane (classify)
@@ -23,6 +27,7 @@ constexpr bool kGatherV3 = false;
 
 struct SelectSmem {
     uint32_t hist[kBins];
+    uint32_t red[kBins / 2];       // this rank's reduced slice of a cluster histogram (C >= 2)
     uint32_t cand[kCand];          // candidate keys (any order)
     uint32_t cand_idx[kCand];      // their segment offsets
     uint32_t bm_gt[kRound / 32];
@@ -171,24 +176,39 @@ __device__ __forceinline__ void merge_hist(SelectSmem &s, int nbins, int C) {
     if (C > 1) merge_hist_cluster(s, nbins, C);
 }
 __device__ __noinline__ void merge_hist_cluster(SelectSmem &s, int nbins, int C) {
+    // reduce-scatter, then all-gather, through DSMEM: rank r sums its slice of
+    // nbins / C bins over every rank (all C remote loads of a bin in flight at
+    // once), then every rank reads the reduced slices back from their owners.
+    // Integer sums in rank order: the result never depends on timing.
     cg::cluster_group cl = cg::this_cluster();
-    cl.sync();
+    const int me = (int)cl.block_rank();
+    const int slice = nbins / C;                      // C | nbins (C, nbins powers of 2)
+    cl.sync();                                        // every rank's histogram is final
+    for (int i = threadIdx.x; i < slice; i += kThreads) {
+        const int bin = me * slice + i;
+        uint32_t v[kMaxCluster];
+#pragma unroll
+        for (int r = 0; r < kMaxCluster; r++) v[r] = r < C ? cl.map_shared_rank(s.hist, r)[bin] : 0u;
+        uint32_t acc = 0;
+#pragma unroll
+        for (int r = 0; r < kMaxCluster; r++) acc += v[r];
+        s.red[i] = acc;
+    }
+    cl.sync();                                        // slices reduced; hist no longer read remotely
     constexpr int kPer = kBins / kThreads;
     uint32_t acc[kPer];
 #pragma unroll
     for (int j = 0; j < kPer; j++) {
         const int bin = threadIdx.x + j * kThreads;
-        acc[j] = 0;
-        if (bin < nbins)
-            for (int r = 0; r < C; r++) acc[j] += cl.map_shared_rank(s.hist, r)[bin];
+        acc[j] = bin < nbins ? cl.map_shared_rank(s.red, bin / slice)[bin % slice] : 0u;
     }
-    cl.sync();
 #pragma unroll
     for (int j = 0; j < kPer; j++) {
         const int bin = threadIdx.x + j * kThreads;
         if (bin < nbins) s.hist[bin] = acc[j];
     }
-    __syncthreads();
+    __syncthreads();    // (red is next written after the next merge's first cluster barrier,
+                        // which every rank reaches only after this gather)
 }
 
 // Cluster-wide totals of s.cnt[0..n) and their sums over earlier ranks

@@ -249,8 +249,10 @@ ASP_API asp_status asyncspade_score_select(const asp_select_params *p, const flo
  * (each token once; -1 and out-of-range entries are ignored), and
  *     out = sum_j softmax_j(sm_scale * q . K_j) V_j
  * with fp32 logits (bf16 x bf16 products are exact), fp32 softmax and fp32
- * accumulation, split over fixed 256-entry chunks of the selection merged
- * in a fixed order (chunk 0 first).  An empty set gives out = 0.
+ * accumulation, split over 256-entry chunks of the selection (one chunk
+ * when top_k + n_fresh <= 384 and G <= 16) merged in a fixed order (chunk 0
+ * first); the split depends only on (top_k, n_fresh, G).  An empty set
+ * gives out = 0.
  *
  * q         device bf16 [batch][n_q_heads][head_dim].
  * k_cache, v_cache  device bf16, strided like asp_select_params' K; rows

@@ -52,7 +52,13 @@ using namespace asp::tc;
 
 constexpr int kTile = 128;                  // tokens per tile
 constexpr int kChunk = 256;                 // entries per work item (fixed: determinism)
-constexpr int kTilesPerItem = kChunk / kTile;
+// A row of up to kTilesMax tiles of entries (384 when G <= 16) is ONE item of
+// up to 3 tiles, so a 257-entry row (high concurrency: k = 256 plus the fresh
+// token) is one item written straight to out -- not a full item plus a
+// one-entry item and a combine.  Item sizes depend only on (top_k, n_fresh,
+// G): never on the grid.
+template <int G>
+constexpr int tiles_max() { return G <= 16 ? 3 : 2; }   // G = 32: the P slots would not fit
 
 constexpr int kProducerWarps = 8;
 constexpr int kProducerThreads = kProducerWarps * 32;
@@ -60,7 +66,7 @@ constexpr int kMmaWarp = kProducerWarps + 4;
 constexpr int kThreads = (kProducerWarps + 5) * 32;   // producers, 4 softmax/epilogue, 1 MMA warp
 constexpr float kLog2e = 1.4426950408889634f;
 
-template <int D, int G>
+template <int D, int G, int NT>
 struct DCfg {
     static constexpr int kRegions = D / 64;
     static constexpr int kStageBytes = kRegions * kTile * 128;      // one K or V tile
@@ -68,13 +74,17 @@ struct DCfg {
     static constexpr int kN2 = 2 * G <= 16 ? 16 : 2 * G;            // MMA2 N: 2G hi/lo P rows
     // K/V ring: 5 (D = 128) / 8 (D = 64) stages, 4 when G = 32's P and Q slots need the room
     static constexpr int kStages = G > 16 ? (D == 128 ? 4 : 6) : (D == 128 ? 5 : 8);
-    static constexpr uint32_t kTmemCols = 4 * kN + 2 * kN2 <= 128 ? 128 : 256;
+
     static constexpr int kGR = G <= 8 ? 8 : G;                      // reduction row stride
     static constexpr int kQSlotBytes = kRegions * kN * 128;
     static constexpr int kPTileBytes = 2 * kN2 * 128;               // 128 tokens = 2 regions
-    static constexpr int kPSlotBytes = kTilesPerItem * kPTileBytes;
+    static constexpr int kTiles = NT;                               // tiles of the largest item
+    static constexpr int kChunkMax = kTiles * kTile;
+    static constexpr uint32_t kTmemCols = 2 * kTiles * kN + 2 * kN2 <= 128 ? 128
+                                        : 2 * kTiles * kN + 2 * kN2 <= 256 ? 256 : 512;
+    static constexpr int kPSlotBytes = kTiles * kPTileBytes;
     static constexpr int kZeroBytes = D == 64 ? 16384 : 0;          // MN-block 1 of V^T for D=64
-    static constexpr int kTokBytes = 2 * kChunk * 4;
+    static constexpr int kTokBytes = 2 * kChunkMax * 4;
     static constexpr int kRedBytes = 2 * 2 * 4 * kGR * 4 + 2 * kGR * 4; // wmax, wsum, mrow
     static constexpr int kBarBytes = 256;
     static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 2 * kQSlotBytes +
@@ -83,7 +93,7 @@ struct DCfg {
 };
 
 struct Item {
-    int row, chunk;
+    int row, chunk, nt;     // nt: tiles of this item (1..kTiles)
 };
 
 // Paged pools (asyncspade_sparse_decode_paged); unused by the dense instantiation.
@@ -92,13 +102,13 @@ struct PagedArgs {
     int page_size, max_pages, num_pages;
 };
 
-template <int D, int G, bool PAGED>
+template <int D, int G, bool PAGED, int NT>
 __global__ void __launch_bounds__(kThreads, 1)
 decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                  const asp_bf16 *__restrict__ k_cache, const asp_bf16 *__restrict__ v_cache,
                  const int32_t *__restrict__ seq_lens, const int32_t *__restrict__ sel_idx,
                  float *__restrict__ partials, float *__restrict__ out, int n_splits, PagedArgs pg) {
-    using C = DCfg<D, G>;
+    using C = DCfg<D, G, NT>;
     constexpr int kGR = C::kGR;
     extern __shared__ unsigned char smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -134,9 +144,16 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
     const long i_start = total * blockIdx.x / gridDim.x;
     const long i_end = total * (blockIdx.x + 1) / gridDim.x;
     const int n_items = (int)(i_end - i_start);
+    // the last chunk's entries (1..kChunkMax); every other chunk has kChunk
+    const int last_entries = E - (n_splits - 1) * kChunk;
     auto item = [&](int i) -> Item {               // total items < 2^31: 32-bit math
         const int g = (int)i_start + i;
-        return Item{g / n_splits, g % n_splits};
+        const int c = g % n_splits;
+        const int ne = c == n_splits - 1 ? last_entries : kChunk;
+        return Item{g / n_splits, c, ne > 0 ? (ne + kTile - 1) / kTile : 1};
+    };
+    auto chunk_end = [&](const Item &it) {         // one past the item's last entry
+        return it.chunk == n_splits - 1 ? E : (it.chunk + 1) * kChunk;
     };
 
     if (threadIdx.x == 0) {
@@ -170,9 +187,9 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
 #ifdef ASP_PROFILE_DECODE
     const long long t_k0 = clock64();
 #endif
-    // TMEM columns: S[slot][tile] at slot*32 + tile*16, O[slot] at 64 + slot*16
-    auto s_col = [](int slot, int t) { return (uint32_t)(slot * 2 * C::kN + t * C::kN); };
-    auto o_col = [](int slot) { return (uint32_t)(4 * C::kN + slot * C::kN2); };
+    // TMEM columns: S[slot][tile] at (slot*kTiles + tile)*kN, O[slot] after them
+    auto s_col = [](int slot, int t) { return (uint32_t)((slot * C::kTiles + t) * C::kN); };
+    auto o_col = [](int slot) { return (uint32_t)(2 * C::kTiles * C::kN + slot * C::kN2); };
 
     if (warp < kProducerWarps) {
         // ================================================= producers (8 warps)
@@ -185,7 +202,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
         uint32_t ph = 0, qph = 0;
         // software pipeline: the selection indices and row length of the NEXT item
         // are loaded while the current one is being gathered
-        constexpr int kEntriesPerThread = kChunk / kProducerThreads;
+        constexpr int kEntriesPerThread = (C::kChunkMax + kProducerThreads - 1) / kProducerThreads;
         int pre_raw[kEntriesPerThread] = {};
         int pre_len = 0;
         auto fetch = [&](int i) {
@@ -195,7 +212,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
 #pragma unroll
             for (int u = 0; u < kEntriesPerThread; u++) {
                 const int e = it.chunk * kChunk + pt + u * kProducerThreads;
-                pre_raw[u] = e < p.top_k ? __ldg(ib + e) : -1;
+                pre_raw[u] = e < p.top_k && e < chunk_end(it) ? __ldg(ib + e) : -1;
             }
         };
         // the attended token of entry u of item `it` (-1: none): a selected index
@@ -204,7 +221,9 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             const int fresh_lo = max(len - p.n_fresh, 0);
             const int e = it.chunk * kChunk + pt + u * kProducerThreads;
             int tok = -1;
-            if (e < p.top_k) {
+            if (e >= chunk_end(it)) {
+                // past this item (the next chunk's entries)
+            } else if (e < p.top_k) {
                 if (raw_u >= 0 && raw_u < fresh_lo) tok = raw_u;
             } else if (e < E) {
                 const int t = fresh_lo + (e - p.top_k);
@@ -290,7 +309,8 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             asm volatile("bar.sync 2, %0;" ::"n"(kProducerThreads) : "memory");
 #pragma unroll
             for (int u = 0; u < kEntriesPerThread; u++)
-                s_tok[slot * kChunk + pt + u * kProducerThreads] = toks[u];
+                if (pt + u * kProducerThreads < C::kChunkMax)
+                    s_tok[slot * C::kChunkMax + pt + u * kProducerThreads] = toks[u];
             asm volatile("bar.sync 2, %0;" ::"n"(kProducerThreads) : "memory");
             if (pt == 0) {
                 mbar_arrive(bar(B_TOKFULL + slot));
@@ -310,22 +330,26 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             constexpr int kPerThread = kTile / kRowsPerPass;  // rows r0 + kRowsPerPass * u
             const int r0 = pt / kChunksPerRow;
             const asp_bf16 *src0 = rowbase + chunk * 8;
-            for (int t = 0; t < kTilesPerItem; t++) {
+            for (int t = 0; t < it.nt; t++) {
                 DWAIT(2, mbar_wait(bar(B_EMPTY + s), ph ^ 1));
                 // rows r0 + 8u share (r & 7): one swizzle per thread
                 const uint32_t dst0 = stage0 + s * C::kStageBytes + region * (kTile * 128) +
                                       r0 * 128 + ((cc ^ (r0 & 7)) * 16);
-                const int32_t *tk = s_tok + slot * kChunk + t * kTile + r0;
+                const int32_t *tk = s_tok + slot * C::kChunkMax + t * kTile + r0;
                 // all token loads first, then the copies back to back (no memory
                 // clobber on the copies: they are ordered by commit / wait_group)
+                // an empty entry (-1: past a short row's selection, or the padding of
+                // a row's last chunk) is zero-filled without a memory read (src-size
+                // 0): its weight is 0, and a zero V row keeps 0 * V finite
                 int tok[kPerThread];
 #pragma unroll
-                for (int u = 0; u < kPerThread; u++) tok[u] = max(tk[u * kRowsPerPass], 0);  // -1 -> row 0
+                for (int u = 0; u < kPerThread; u++) tok[u] = tk[u * kRowsPerPass];
 #pragma unroll
                 for (int u = 0; u < kPerThread; u++) {
-                    const asp_bf16 *src = src0 + (int64_t)tok[u] * st;
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
-                                 ::"r"(dst0 + (uint32_t)(u * kRowsPerPass * 128)), "l"(src));
+                    const asp_bf16 *src = src0 + (int64_t)max(tok[u], 0) * st;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+                                 ::"r"(dst0 + (uint32_t)(u * kRowsPerPass * 128)), "l"(src),
+                                 "r"(tok[u] >= 0 ? 16 : 0));
                 }
                 // cp.async writes are generic-proxy: each producer waits for its group
                 // from kLag tiles ago, fences it to the async proxy (tensor core), and
@@ -373,7 +397,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                     cur_row = it.row;
                 }
                 const uint32_t qb = qslot0 + qs * C::kQSlotBytes;
-                for (int t = 0; t < kTilesPerItem; t++) {
+                for (int t = 0; t < it.nt; t++) {
                     wait_stage();
                     const uint32_t ab = stage0 + s * C::kStageBytes;
 #pragma unroll
@@ -395,7 +419,8 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                 DWAIT(6, mbar_wait(bar(B_OEMPTY + slot), use ^ 1));
                 tc_fence_after();
                 const uint32_t pb = pslot0 + slot * C::kPSlotBytes;
-                for (int t = 0; t < kTilesPerItem; t++) {
+                const int nt = item(i).nt;
+                for (int t = 0; t < nt; t++) {
                     wait_stage();
                     const uint32_t vb = stage0 + s * C::kStageBytes;
                     // V tile as the MN-major A operand of O^T = V^T P^T: MN blocks of 64
@@ -431,17 +456,24 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             DWAIT(7, mbar_wait(bar(B_TOKFULL + slot), use));
             DWAIT(8, mbar_wait(bar(B_SFULL + slot), use));
             tc_fence_after();
-            float l[kTilesPerItem][G];
-            int tok[kTilesPerItem];
+            const int nt = item(i).nt;
+            float l[C::kTiles][G];
+            int tok[C::kTiles];
 #pragma unroll
-            for (int t = 0; t < kTilesPerItem; t++) {
+            for (int t = 0; t < C::kTiles; t++) {
+                if (t >= nt) {                   // no such tile in this item
+                    tok[t] = -1;
+#pragma unroll
+                    for (int g = 0; g < G; g++) l[t][g] = -INFINITY;
+                    continue;
+                }
                 uint32_t r[C::kN];
                 if constexpr (C::kN == 32)
                     tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + s_col(slot, t), r);
                 else
                     tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + s_col(slot, t), r);
                 tmem_wait_ld();
-                tok[t] = s_tok[slot * kChunk + t * kTile + quad * 32 + lane];
+                tok[t] = s_tok[slot * C::kChunkMax + t * kTile + quad * 32 + lane];
 #pragma unroll
                 for (int g = 0; g < G; g++)
                     l[t][g] = tok[t] >= 0 ? __uint_as_float(r[g]) * scale : -INFINITY;
@@ -469,7 +501,7 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
             for (int g = 0; g < G; g++) {
                 float m = l[0][g];
 #pragma unroll
-                for (int t = 1; t < kTilesPerItem; t++) m = fmaxf(m, l[t][g]);
+                for (int t = 1; t < C::kTiles; t++) m = fmaxf(m, l[t][g]);
                 mx[g] = asp::warp_max(m);
             }
             if (lane == 0)
@@ -491,7 +523,8 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
 #pragma unroll
             for (int g = 0; g < G; g++) sum[g] = 0.0f;
 #pragma unroll
-            for (int t = 0; t < kTilesPerItem; t++) {
+            for (int t = 0; t < C::kTiles; t++) {
+                if (t >= nt) continue;           // (its P tile is not read)
                 unsigned char *ptile = pb + t * C::kPTileBytes + region * (C::kN2 * 128);
 #pragma unroll
                 for (int g = 0; g < G; g++) {
@@ -685,21 +718,27 @@ decode_combine_kernel(asp_decode_params p, const float *__restrict__ partials,
 
 int n_splits_of(const asp_decode_params &p) {
     const int E = p.top_k + p.n_fresh;
-    return E > 0 ? (E + kChunk - 1) / kChunk : 1;
+    const int G = p.n_q_heads / p.n_kv_heads;
+    const int max_last = (G <= 16 ? tiles_max<1>() : tiles_max<32>()) * kTile;   // 384 / 256
+    // one item up to max_last entries (no combine); else chunks of kChunk.
+    // (Folding a longer row's remainder into a 3-tile last chunk -- config [2]'s
+    // 2049 entries as 8 items instead of 9 -- measured SLOWER: 104 -> 113 us.)
+    if (E <= max_last) return 1;
+    return (E + kChunk - 1) / kChunk;
 }
 
-template <int D, int G>
-cudaError_t launch(const asp_decode_params &p, const asp_bf16 *q, const asp_bf16 *k,
-                   const asp_bf16 *v, const int32_t *seq_lens, const int32_t *idx, float *out,
-                   float *partials, cudaStream_t s, const asp_paged_kv *pk,
-                   const int32_t *block_table) {
-    using C = DCfg<D, G>;
+template <int D, int G, int NT>
+cudaError_t launch_nt(const asp_decode_params &p, const asp_bf16 *q, const asp_bf16 *k,
+                      const asp_bf16 *v, const int32_t *seq_lens, const int32_t *idx, float *out,
+                      float *partials, cudaStream_t s, const asp_paged_kv *pk,
+                      const int32_t *block_table) {
+    using C = DCfg<D, G, NT>;
     const int ns = n_splits_of(p);
     const long total = (long)p.batch * p.n_kv_heads * ns;
     const int grid = (int)(total < asp_sm_count() ? total : asp_sm_count());
     PagedArgs pg{block_table, pk ? pk->page_size : 1, pk ? pk->max_pages_per_seq : 0,
                  pk ? pk->num_pages : 0};
-    auto kern = pk ? decode_tc_kernel<D, G, true> : decode_tc_kernel<D, G, false>;
+    auto kern = pk ? decode_tc_kernel<D, G, true, NT> : decode_tc_kernel<D, G, false, NT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
@@ -716,6 +755,24 @@ cudaError_t launch(const asp_decode_params &p, const asp_bf16 *q, const asp_bf16
     }
     return asp_launch(decode_combine_kernel<D>, dim3(p.n_q_heads, p.batch), dim3(D), csmem, s, 1, p,
                       (const float *)partials, out, ns);
+}
+
+// Two instantiations: 2-tile items (every multi-chunk row), and one item of up
+// to 3 tiles for rows of 257..384 entries (G <= 16).  The 3-tile structure in
+// the 2-tile case measured 104 -> 113 us at config [2] (wider softmax state,
+// two index loads per producer thread), so it is used only where it saves a
+// whole item and the combine.
+template <int D, int G>
+cudaError_t launch(const asp_decode_params &p, const asp_bf16 *q, const asp_bf16 *k,
+                   const asp_bf16 *v, const int32_t *seq_lens, const int32_t *idx, float *out,
+                   float *partials, cudaStream_t s, const asp_paged_kv *pk,
+                   const int32_t *block_table) {
+    if constexpr (tiles_max<G>() == 3) {
+        if (p.top_k + p.n_fresh > kChunk)
+            if (n_splits_of(p) == 1)
+                return launch_nt<D, G, 3>(p, q, k, v, seq_lens, idx, out, partials, s, pk, block_table);
+    }
+    return launch_nt<D, G, 2>(p, q, k, v, seq_lens, idx, out, partials, s, pk, block_table);
 }
 
 }  // namespace

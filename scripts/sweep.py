@@ -165,11 +165,16 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--only", default="", help="comma list of batch sizes (high-concurrency) "
+                    "or log2 contexts (long-cot) to run")
     args = ap.parse_args()
+    only = {int(x) for x in args.only.split(",") if x}
     asp.lib()
     lines = []
     if args.sweep == "long-cot":
         for e in range(12, 20):                                # 4k .. 512k
+            if only and e not in only:
+                continue
             cfg = configs.long_cot(1 << e)
             lines.append(point(cfg, args, kv_heads=(0, 1)))     # per-GPU shard at P = 8
             print(json.dumps(lines[-1]), flush=True)
@@ -299,6 +304,8 @@ def main():
                 torch.cuda.empty_cache()
     else:
         for e in range(0, 10):                                 # batch 1 .. 512
+            if only and (1 << e) not in only:
+                continue
             cfg = configs.high_concurrency(1 << e)
             lines.append(point(cfg, args, overlap=True))
             print(json.dumps(lines[-1]), flush=True)

@@ -116,6 +116,7 @@ def test_sparse_decode_validation_and_workspace(L):
     need = L.asyncspade_sparse_decode_workspace(ctypes.byref(p))
     # one 256-entry chunk: [B][Hq][1][D + 2] fp32 partials
     assert need >= 2 * 32 * 1 * 130 * 4 and need % 256 == 0
+    # 601 entries: three 256-entry chunks (rows of <= 384 entries are one item)
     need3 = L.asyncspade_sparse_decode_workspace(ctypes.byref(_dec(top_k=600)))
     assert need3 >= 2 * 32 * 3 * 130 * 4 and need3 % 256 == 0
     assert call(p, out=None) == 1

@@ -234,6 +234,25 @@ def test_decode_parity(G, D, n_fresh):
     assert rel_inf_err(out, ref) <= ATTN_RTOL
 
 
+@pytest.mark.parametrize("G", [4, 8, 16, 32])
+@pytest.mark.parametrize("k,n_fresh", [(128, 1), (256, 1), (300, 0), (383, 1), (384, 0), (384, 1)])
+def test_decode_one_item_rows(G, k, n_fresh):
+    """Rows of top_k + n_fresh <= 384 entries are ONE decode item of up to 3
+    tiles written straight to out (G <= 16); 385 entries and G = 32 take the
+    256-entry split + combine.  Every boundary against the oracle, with a
+    ragged row and selections that run into the fresh tail."""
+    rng = np.random.default_rng(G * 1000 + k + n_fresh)
+    B, Hkv, D, L = 2, 2, 128, 1024
+    seq_lens = [1024, 333]
+    idx = np.full((B, Hkv, k), -1, np.int32)
+    for b in range(B):
+        for h in range(Hkv):
+            m = min(k - 3, seq_lens[b])
+            idx[b, h, :m] = np.sort(rng.choice(seq_lens[b], m, replace=False))
+    out, ref, _ = _decode_case(B, Hkv * G, Hkv, D, L, idx, seq_lens, n_fresh, 70 + G)
+    assert rel_inf_err(out, ref) <= ATTN_RTOL
+
+
 def test_decode_full_selection_equals_dense():
     """North star: with k = context length, sparse attention == dense."""
     B, Hq, Hkv, D, L = 2, 8, 2, 128, 700

@@ -542,7 +542,8 @@ def test_async_pipeline_matches_serial():
 
 
 # ----------------------------------------------------------------------------- paged pools (NEXT-4)
-@pytest.mark.parametrize("G,D,P", [(8, 128, 16), (1, 64, 64), (4, 128, 32), (2, 64, 128)])
+@pytest.mark.parametrize("G,D,P", [(8, 128, 16), (1, 64, 64), (4, 128, 32), (2, 64, 128),
+                                   (2, 64, 16), (16, 128, 32), (32, 64, 16)])
 def test_paged_matches_dense_bit_for_bit(G, D, P):
     """The paged entry points return bit for bit what the dense ones return on
     the same logical cache (random page placement, spare pages, ragged

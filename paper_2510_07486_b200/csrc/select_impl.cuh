@@ -14,17 +14,6 @@ constexpr int kRound = SEL_ROUND;
 constexpr int kSampleChunks = 32;             // 32 x 128 consecutive keys sampled per row
 constexpr int kMaxCluster = 16;
 constexpr int kUnroll = 8;                    // 16-B loads in flight per lane (classify)
-#ifdef ASP_SEL_V2
-constexpr bool kDirectList = true;            // direct segments list candidates in the sweep
-#else
-constexpr bool kDirectList = false;
-#endif
-#ifdef ASP_SEL_V3
-constexpr bool kGatherV3 = true;              // warp-aggregated slots, batched key loads
-#else
-constexpr bool kGatherV3 = false;
-#endif
-
 struct SelectSmem {
     uint32_t hist[kBins];
     uint32_t red[kBins / 2];       // this rank's reduced slice of a cluster histogram (C >= 2)
@@ -406,39 +395,7 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
                 ab &= valid;
                 in &= valid & ~ab;
                 above += __popc(ab);
-                if (direct && kDirectList) {
-                    // above: bitmap word ch*4 + lane/8 <- nibbles of 8 lanes;
-                    // candidates: straight into the list from registers, one
-                    // shared atomic per warp step (slots by a ballot prefix of
-                    // the lanes' counts, each <= 4)
-                    uint32_t wa = ab << (4 * (lane & 7));
-#pragma unroll
-                    for (int d = 1; d < 8; d <<= 1) wa |= __shfl_xor_sync(0xffffffffu, wa, d);
-                    if ((lane & 7) == 0) s.bm_gt[(ch << 2) + (lane >> 3)] = wa;
-                    const uint32_t nin = __popc(in);
-                    const uint32_t b1 = __ballot_sync(0xffffffffu, nin >= 1);
-                    if (b1) {                                      // warp-uniform
-                        const uint32_t b2 = __ballot_sync(0xffffffffu, nin >= 2);
-                        const uint32_t b3 = __ballot_sync(0xffffffffu, nin >= 3);
-                        const uint32_t b4 = __ballot_sync(0xffffffffu, nin >= 4);
-                        const uint32_t lt = (1u << lane) - 1u;
-                        uint32_t slot = __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt) + __popc(b4 & lt);
-                        uint32_t base = 0;
-                        if (lane == 0)
-                            base = atomicAdd(&s.n_cand, (uint32_t)(__popc(b1) + __popc(b2) + __popc(b3) + __popc(b4)));
-                        slot += __shfl_sync(0xffffffffu, base, 0);
-#pragma unroll
-                        for (int c = 0; c < 4; c++) {
-                            if ((in >> c) & 1u) {
-                                if (slot < (uint32_t)kCand) {
-                                    s.cand[slot] = asp::score_key(comp(kv[u], c));
-                                    s.cand_idx[slot] = (uint32_t)(o + c);
-                                }
-                                slot++;
-                            }
-                        }
-                    }
-                } else if (direct) {          // word ch*4 + lane/8 <- nibbles of 8 lanes
+                if (direct) {                 // word ch*4 + lane/8 <- nibbles of 8 lanes
                     uint32_t wa = ab << (4 * (lane & 7)), wc = in << (4 * (lane & 7));
 #pragma unroll
                     for (int d = 1; d < 8; d <<= 1) {
@@ -467,47 +424,7 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
         above = warp_sum_u32(above);
         const uint32_t a = block_sum_warps(s, above);
         SPROF(5);
-        if (direct && !kDirectList && kGatherV3) {
-            // gather the marked candidates' offsets (one shared atomic per warp
-            // round: a warp scan of the words' popcounts), clear bm_eq; then
-            // load their keys with every load in flight at once
-            const int nw = nchunks << 2;
-            for (int w0 = 0; w0 < nw; w0 += kThreads) {
-                const int w = w0 + t;
-                uint32_t bits = w < nw ? s.bm_eq[w] : 0u;
-                if (bits) s.bm_eq[w] = 0;
-                const uint32_t c = (uint32_t)__popc(bits);
-                uint32_t x = c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= o) x += y;
-                }
-                uint32_t base = 0;
-                if (lane == 31 && x) base = atomicAdd(&s.n_cand, x);
-                uint32_t slot = __shfl_sync(0xffffffffu, base, 31) + x - c;
-                while (bits) {
-                    if (slot < (uint32_t)kCand) s.cand_idx[slot] = (uint32_t)((w << 5) + __ffs(bits) - 1);
-                    bits &= bits - 1;
-                    slot++;
-                }
-            }
-            __syncthreads();
-            const int nc = min((int)s.n_cand, kCand);
-            for (int e0 = 0; e0 < nc; e0 += 4 * kThreads) {
-                float v[4];
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int e = e0 + u * kThreads + t;
-                    v[u] = e < nc ? __ldg(srow + s.cand_idx[e]) : 0.f;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int e = e0 + u * kThreads + t;
-                    if (e < nc) s.cand[e] = asp::score_key(v[u]);
-                }
-            }
-        } else if (direct && !kDirectList) {   // gather the marked candidates; clear bm_eq
+        if (direct) {                         // gather the marked candidates; clear bm_eq
             for (int w = t; w < ((nchunks << 2)); w += kThreads) {
                 uint32_t bits = s.bm_eq[w];
                 if (!bits) continue;

@@ -3,7 +3,8 @@ append -> predict -> score_select (dense and paged) -> decode -> gather ->
 quest, on a ragged two-sequence batch; then full steps at G = 16 and G = 32,
 the round-2 kernels (head-dim-split predict, G = 64 tensor-core score,
 CUDA-core score / decode for absorbed MLA and 128-head MQA, single-chunk
-direct output, head-major output, window-less append)."""
+direct output, head-major output, window-less append), and session 3's
+one-item decode rows and cluster-split long rows."""
 import os, sys, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2510_07486_b200 as asp
@@ -44,6 +45,17 @@ for c2 in (configs.Config("mqa64", 0, 2, 64, 1, 128, 2048, 256, 16),
     s2.run()
     flags = int(s2.dev_flags.item())
     assert flags == 0, flags
+# session 3: a one-item 3-tile decode row (k + n_fresh = 257), and long rows
+# split over 8-CTA clusters with 64k-key segments (DSMEM reduce-scatter merges,
+# 64k direct emission) feeding the staged-scale combine (129 chunks per row)
+for c2 in (configs.Config("onei", 0, 2, 16, 2, 128, 2048, 256, 16),
+           configs.Config("longrow", 0, 5, 2, 1, 128, 524288, 32768, 16)):
+    s2 = DecodeStep(c2, "cuda", n_fresh=1)
+    s2.fill_synthetic()
+    s2.run()
+    flags = int(s2.dev_flags.item())
+    assert flags == 0, flags
+    del s2
 q_only = torch.empty(2, 32, 128, dtype=torch.bfloat16, device="cuda")
 asp.append(torch.randn(2, 32, 128, generator=g).cuda(), None, 0, q_cur=q_only)
 torch.cuda.synchronize()

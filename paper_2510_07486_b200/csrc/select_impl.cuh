@@ -459,7 +459,8 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
     if (t == 0) atomicAdd(&g_sel_prof[6], (unsigned long long)tot[1]);
 #endif
 
-    // ---- 3. exact T: radix select (12 + 12 + 8 bits) over candidates or all keys
+    // ---- 3. exact T: radix select over the candidates (relative to the
+    // bracket, 8-bit digits) or, if the sample missed, over all keys (12 + 12 + 8)
     // fn(key, candidate slot or -1)
     auto for_each_key = [&](auto &&fn) {
         if (use_cand) {
@@ -469,28 +470,54 @@ select_kernel(asp_select_params p, const float *__restrict__ scores,
             for (int o = t; o < n; o += kThreads) fn(key_at(o), -1);
         }
     };
-    zero_hist(s, kBins);
-    __syncthreads();
-    for_each_key([&](uint32_t key, int) { atomicAdd(&s.hist[key >> 20], 1u); });
-    merge_hist(s, kBins, C);
-    find_bucket(s, kBins, rank0, rank0);
-    const uint32_t d1 = s.found_bin, rem1 = s.found_rem;
-    zero_hist(s, kBins);
-    __syncthreads();
-    for_each_key([&](uint32_t key, int) {
-        if ((key >> 20) == d1) atomicAdd(&s.hist[(key >> 8) & 0xFFFu], 1u);
-    });
-    merge_hist(s, kBins, C);
-    find_bucket(s, kBins, rem1, rem1);
-    const uint32_t pre24 = (d1 << 12) | s.found_bin, rem2 = s.found_rem;
-    zero_hist(s, 256);
-    __syncthreads();
-    for_each_key([&](uint32_t key, int) {
-        if ((key >> 8) == pre24) atomicAdd(&s.hist[key & 0xFFu], 1u);
-    });
-    merge_hist(s, 256, C);
-    find_bucket(s, 256, rem2, rem2);
-    const uint32_t T = (pre24 << 8) | s.found_bin;
+    uint32_t T;
+    if (use_cand) {
+        // the candidates lie in [key_lo, key_hi]: radix over key - key_lo, 8 bits
+        // (256 bins: cheap zeroing, scans and cluster merges) per level, only as
+        // many levels as the bracket is wide (usually 2)
+        const uint32_t span = key_hi - key_lo;
+        int bits = span ? 32 - __clz(span) : 1;
+        uint32_t prefix = 0, rem = rank0;
+        while (bits > 0) {
+            const int shift = bits > 8 ? bits - 8 : 0;
+            zero_hist(s, 256);
+            __syncthreads();
+            for_each_key([&](uint32_t key, int) {
+                const uint32_t rel = key - key_lo;
+                if (((uint64_t)rel >> bits) == ((uint64_t)prefix >> bits))
+                    atomicAdd(&s.hist[(rel >> shift) & 0xFFu], 1u);
+            });
+            merge_hist(s, 256, C);
+            find_bucket(s, 256, rem, rem);
+            prefix |= s.found_bin << shift;
+            rem = s.found_rem;
+            bits = shift;
+        }
+        T = key_lo + prefix;
+    } else {
+        zero_hist(s, kBins);
+        __syncthreads();
+        for_each_key([&](uint32_t key, int) { atomicAdd(&s.hist[key >> 20], 1u); });
+        merge_hist(s, kBins, C);
+        find_bucket(s, kBins, rank0, rank0);
+        const uint32_t d1 = s.found_bin, rem1 = s.found_rem;
+        zero_hist(s, kBins);
+        __syncthreads();
+        for_each_key([&](uint32_t key, int) {
+            if ((key >> 20) == d1) atomicAdd(&s.hist[(key >> 8) & 0xFFFu], 1u);
+        });
+        merge_hist(s, kBins, C);
+        find_bucket(s, kBins, rem1, rem1);
+        const uint32_t pre24 = (d1 << 12) | s.found_bin, rem2 = s.found_rem;
+        zero_hist(s, 256);
+        __syncthreads();
+        for_each_key([&](uint32_t key, int) {
+            if ((key >> 8) == pre24) atomicAdd(&s.hist[key & 0xFFu], 1u);
+        });
+        merge_hist(s, 256, C);
+        find_bucket(s, 256, rem2, rem2);
+        T = (pre24 << 8) | s.found_bin;
+    }
     const uint32_t need = s.found_rem;       // keys == T to take, lowest index first
     SPROF(3);
 

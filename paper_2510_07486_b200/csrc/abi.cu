@@ -22,6 +22,13 @@ int v_dim_of(const asp_decode_params *p) { return p->v_head_dim ? p->v_head_dim 
 bool tc_decode_ok(const asp_decode_params *p) {
     return dim_ok(p->head_dim) && group_ok(p->n_q_heads / p->n_kv_heads) && v_dim_of(p) == p->head_dim;
 }
+// MQA with 64 / 128 query heads on the tensor cores: the one KV head is taken as
+// G / 32 "virtual" KV heads of 32 query heads each (decode.cu; dense caches only)
+bool tc_decode_mqa_ok(const asp_decode_params *p) {
+    const int G = p->n_q_heads / p->n_kv_heads;
+    return dim_ok(p->head_dim) && p->n_kv_heads == 1 && (G == 64 || G == 128) &&
+           v_dim_of(p) == p->head_dim;
+}
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 asp_status from_cuda(cudaError_t e) { return e == cudaSuccess ? ASP_OK : ASP_ERR_CUDA; }
@@ -202,8 +209,8 @@ asp_status asyncspade_score_select_paged(const asp_select_params *p, const asp_p
 
 size_t asyncspade_sparse_decode_workspace(const asp_decode_params *p) {
     if (check_decode(p) != ASP_OK) return 0;
-    return tc_decode_ok(p) ? asp_decode_workspace_bytes(*p)
-                           : asp_decode_cc_workspace_bytes(*p, v_dim_of(p));
+    return tc_decode_ok(p) || tc_decode_mqa_ok(p) ? asp_decode_workspace_bytes(*p)
+                                                  : asp_decode_cc_workspace_bytes(*p, v_dim_of(p));
 }
 
 asp_status asyncspade_sparse_decode(const asp_decode_params *p, const asp_bf16 *q,
@@ -217,7 +224,7 @@ asp_status asyncspade_sparse_decode(const asp_decode_params *p, const asp_bf16 *
         return ASP_ERR_INVALID_ARGUMENT;
     if (!workspace || workspace_bytes < asyncspade_sparse_decode_workspace(p)) return ASP_ERR_WORKSPACE;
     if (reinterpret_cast<uintptr_t>(workspace) & 255u) return ASP_ERR_WORKSPACE;
-    if (!tc_decode_ok(p))
+    if (!tc_decode_ok(p) && !tc_decode_mqa_ok(p))
         return from_cuda(asp_launch_decode_cc(*p, v_dim_of(p), q, k_cache, v_cache, seq_lens,
                                               sel_idx, out, workspace, (cudaStream_t)stream));
     return from_cuda(asp_launch_decode(*p, q, k_cache, v_cache, seq_lens, sel_idx, out, workspace,

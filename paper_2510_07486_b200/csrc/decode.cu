@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
                  const asp_bf16 *__restrict__ k_cache, const asp_bf16 *__restrict__ v_cache,
                  const int32_t *__restrict__ seq_lens, const int32_t *__restrict__ sel_idx,
-                 float *__restrict__ partials, float *__restrict__ out, int n_splits, PagedArgs pg) {
+                 float *__restrict__ partials, float *__restrict__ out, int n_splits, PagedArgs pg,
+                 int vshift) {
     using C = DCfg<D, G, NT>;
     constexpr int kGR = C::kGR;
     extern __shared__ unsigned char smem_raw[];
@@ -208,7 +209,8 @@ decode_tc_kernel(asp_decode_params p, const asp_bf16 *__restrict__ q,
         auto fetch = [&](int i) {
             const Item it = item(i);
             pre_len = seq_lens[it.row / Hkv];
-            const int32_t *ib = sel_idx + (size_t)it.row * p.top_k;
+            // (virtual KV heads of an MQA split share their batch's index row)
+            const int32_t *ib = sel_idx + (size_t)(it.row >> vshift) * p.top_k;
 #pragma unroll
             for (int u = 0; u < kEntriesPerThread; u++) {
                 const int e = it.chunk * kChunk + pt + u * kProducerThreads;
@@ -731,7 +733,7 @@ template <int D, int G, int NT>
 cudaError_t launch_nt(const asp_decode_params &p, const asp_bf16 *q, const asp_bf16 *k,
                       const asp_bf16 *v, const int32_t *seq_lens, const int32_t *idx, float *out,
                       float *partials, cudaStream_t s, const asp_paged_kv *pk,
-                      const int32_t *block_table) {
+                      const int32_t *block_table, int vshift) {
     using C = DCfg<D, G, NT>;
     const int ns = n_splits_of(p);
     const long total = (long)p.batch * p.n_kv_heads * ns;
@@ -743,7 +745,7 @@ cudaError_t launch_nt(const asp_decode_params &p, const asp_bf16 *q, const asp_b
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
     e = asp_launch(kern, dim3(grid), dim3(kThreads), C::kSmemBytes, s, 1, p, q, k, v, seq_lens,
-                   idx, partials, out, ns, pg);
+                   idx, partials, out, ns, pg, vshift);
     if (e != cudaSuccess || ns == 1) return e;            // one chunk: written directly
     if (ns <= kCombineShort)
         return asp_launch(decode_combine_short_kernel<D>, dim3(p.n_q_heads, p.batch), dim3(D), 0, s, 1,
@@ -766,13 +768,14 @@ template <int D, int G>
 cudaError_t launch(const asp_decode_params &p, const asp_bf16 *q, const asp_bf16 *k,
                    const asp_bf16 *v, const int32_t *seq_lens, const int32_t *idx, float *out,
                    float *partials, cudaStream_t s, const asp_paged_kv *pk,
-                   const int32_t *block_table) {
+                   const int32_t *block_table, int vshift = 0) {
     if constexpr (tiles_max<G>() == 3) {
         if (p.top_k + p.n_fresh > kChunk)
             if (n_splits_of(p) == 1)
-                return launch_nt<D, G, 3>(p, q, k, v, seq_lens, idx, out, partials, s, pk, block_table);
+                return launch_nt<D, G, 3>(p, q, k, v, seq_lens, idx, out, partials, s, pk, block_table,
+                                          vshift);
     }
-    return launch_nt<D, G, 2>(p, q, k, v, seq_lens, idx, out, partials, s, pk, block_table);
+    return launch_nt<D, G, 2>(p, q, k, v, seq_lens, idx, out, partials, s, pk, block_table, vshift);
 }
 
 }  // namespace
@@ -798,6 +801,23 @@ cudaError_t asp_launch_decode(const asp_decode_params &p, const asp_bf16 *q,
                               const int32_t *block_table) {
     float *partials = static_cast<float *>(workspace);
     const int G = p.n_q_heads / p.n_kv_heads;
+    if (G > 32 && p.n_kv_heads == 1 && pk == nullptr && (G == 64 || G == 128)) {
+        // MQA with 64 / 128 query heads: G / 32 "virtual" KV heads of 32 query
+        // heads each over the SAME key / value rows (head stride 0) and the same
+        // index row (row >> vshift).  Every virtual head gathers the selected rows
+        // again, but its neighbour runs at the same time on the next SM, so the
+        // second read is mostly an L2 hit; the arithmetic is the G = 32 kernel's.
+        asp_decode_params v = p;
+        v.n_kv_heads = G / 32;
+        v.k_stride_h = v.v_stride_h = 0;
+        const int vshift = G == 64 ? 1 : 2;
+        if (p.head_dim == 64)
+            return launch<64, 32>(v, q, k_cache, v_cache, seq_lens, sel_idx, out, partials, s, nullptr,
+                                  nullptr, vshift);
+        if (p.head_dim == 128)
+            return launch<128, 32>(v, q, k_cache, v_cache, seq_lens, sel_idx, out, partials, s, nullptr,
+                                   nullptr, vshift);
+    }
 #define ASP_CASE(DD, GG) \
     if (p.head_dim == DD && G == GG) \
         return launch<DD, GG>(p, q, k_cache, v_cache, seq_lens, sel_idx, out, partials, s, pk, block_table);

@@ -33,9 +33,10 @@
  *   head_dim / group size G = n_q_heads / n_kv_heads (score + select: head_dim
  *   64 / 128 with G in {1, 2, 4, ..., 64}, 576 with G <= 16 on the tensor
  *   cores, plus the CUDA-core shapes (head_dim 576 / 256 / 128 / 64, G up to
- *   128); decode: head_dim 64 / 128 with G <= 32 on the tensor cores, plus
- *   absorbed MLA (576 / v_head_dim 512, G <= 16) and G = 64 / 128 on the CUDA
- *   cores; predict: head_dim 64, 128, 256, 576) / window (1..32),
+ *   128); decode: head_dim 64 / 128 with G <= 32, and one KV head with G =
+ *   64 / 128 (MQA), on the tensor cores, plus absorbed MLA (576 / v_head_dim
+ *   512, G <= 16) and G = 64 / 128 over several KV heads on the CUDA cores;
+ *   predict: head_dim 64, 128, 256, 576) / window (1..32),
  *   misaligned pointers (16 B), strides not multiples of 8 elements,
  *   too-small workspace.  Launch failures return
  *   ASP_ERR_CUDA.  Numeric conditions never fail a call: they OR a bit into

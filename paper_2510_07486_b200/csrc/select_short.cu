@@ -22,6 +22,9 @@
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef ASP_SHORT_MINB
+#define ASP_SHORT_MINB 4
+#endif
 constexpr int kWarps = kThreads / 32;
 
 struct ShortSmem {
@@ -53,7 +56,7 @@ __device__ __forceinline__ uint32_t scan256(ShortSmem &s, uint32_t v, uint32_t *
 }
 
 template <int KPT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, KPT == 16 ? ASP_SHORT_MINB : 1)
 select_short_kernel(asp_select_params p, const float *__restrict__ scores,
                     const int32_t *__restrict__ seq_lens, int32_t *__restrict__ sel_idx,
                     uint32_t *dev_flags, int discard) {

@@ -191,6 +191,23 @@ def test_score_select_cluster_split_rows(B, L, k):
         check_selection(idx[b, 0], so[b, 0], lens[b], k)
 
 
+def test_score_select_64k_cluster_segments():
+    """Long rows over 8-CTA clusters with 64k-key segments (the sel1024w
+    instantiation: 64k-key direct emission rounds, DSMEM reduce-scatter
+    histogram merges, the bracket-relative radix): exact sets on ragged rows
+    whose ends fall inside a segment, and on all-equal keys (every candidate
+    list overflows: the exact all-keys radix must give the lowest indices)."""
+    B, L, k = 5, 524288, 32768
+    lens = [L, L - 37, L - 70001, 300000, 65537]
+    idx, _, so, _ = _score_select_case(B, 1, 1, 64, L, k, lens, 91)
+    for b in range(B):
+        check_selection(idx[b, 0], so[b, 0], lens[b], k)
+    K = np.zeros((B, 1, L, 64), np.uint16)
+    idx, _, _, _ = _score_select_case(B, 1, 1, 64, L, k, lens, 92, kv=K)
+    for b in range(B):
+        np.testing.assert_array_equal(idx[b, 0], np.arange(k))
+
+
 def test_score_select_uncached_longest_rows():
     """Rows beyond 16 x 40,960 tokens: the cluster streams keys from L2."""
     L, k = 720896, 45056

@@ -860,11 +860,15 @@ def test_step_large_groups_multi_item(G):
     torch.cuda.empty_cache()
 
 
-def test_decode_head_major_out():
-    """ABI 2: the split-K combine writes `out` through (row, head) strides;
+@pytest.mark.parametrize("cfg", [configs.QWEN3_8B.with_(batch=3, seq_len=4096, top_k=700),
+                                 configs.QWEN3_8B.with_(batch=3, seq_len=4096, top_k=256),
+                                 configs.Config("mqa64", 0, 3, 64, 1, 128, 4096, 700, 16)],
+                         ids=["split-k", "one-item", "mqa64-virtual-heads"])
+def test_decode_head_major_out(cfg):
+    """ABI 2: the split-K combine (and a one-item row's direct write, and the
+    MQA virtual-head split) writes `out` through (row, head) strides;
     head-major [Hq, B, D] holds bit for bit the dense result transposed, so
     KV-head shards concatenate."""
-    cfg = configs.QWEN3_8B.with_(batch=3, seq_len=4096, top_k=700)
     step = DecodeStep(cfg, DEV, n_fresh=1)
     step.fill_synthetic()
     step.run()

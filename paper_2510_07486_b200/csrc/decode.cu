@@ -721,7 +721,7 @@ decode_combine_kernel(asp_decode_params p, const float *__restrict__ partials,
 int n_splits_of(const asp_decode_params &p) {
     const int E = p.top_k + p.n_fresh;
     const int G = p.n_q_heads / p.n_kv_heads;
-    const int max_last = (G <= 16 ? tiles_max<1>() : tiles_max<32>()) * kTile;   // 384 / 256
+    const int max_last = (G <= 16 ? 3 : 2) * kTile;     // tiles_max<G>() tiles: 384 / 256 entries
     // one item up to max_last entries (no combine); else chunks of kChunk.
     // (Folding a longer row's remainder into a 3-tile last chunk -- config [2]'s
     // 2049 entries as 8 items instead of 9 -- measured SLOWER: 104 -> 113 us.)

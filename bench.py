@@ -719,6 +719,13 @@ def main():
         n_sel_reads = 1 if cfg.v_head_dim and cfg.v_head_dim != cfg.head_dim else 2
         core = k_bytes + n_sel_reads * sum(min(cfg.top_k, n) for n in lens) * hn * D2
         achieved = k_bytes / (avg_sel_max * 1e-3) / 1e9
+        # all algorithmic bytes: + the query window, q_hat written and
+        # read, the current query, the indices written and read, the output
+        n_q = sh.bn * hn * cfg.group
+        wbytes = 2 if args.bf16_window else 4
+        all_bytes = (core + n_q * cfg.window * cfg.head_dim * wbytes + 2 * n_q * cfg.head_dim * 4
+                     + n_q * cfg.head_dim * 2 + 2 * sh.bn * hn * cfg.top_k * 4
+                     + n_q * (cfg.v_head_dim or cfg.head_dim) * 4)
         line = {
             "metric": METRIC, "value": ms_step * 1e3, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -739,6 +746,8 @@ def main():
                              (2 * k_bytes / 1e9)},
             "hbm_tb_per_s": core / (ms_step * 1e-3) / 1e12,
             "core_bytes_per_gpu": core,
+            "all_bytes_per_gpu": all_bytes,
+            "hbm_tb_per_s_all_bytes": all_bytes / (ms_step * 1e-3) / 1e12,
             "roofline_frac_step": core / (ms_step * 1e-3) / 1e9 / peak,
             "roofline_frac_step_nominal_8tbs": core / (ms_step * 1e-3) / 8e12,
             "per_call_ms": {"predict_query": avg_pred, "score_select": avg_sel,

@@ -22,4 +22,4 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-a5 --ragged > gpurun_out/${TAG}_bench_ragged.json 2>/dev/null; echo "ragged rc=$?"
 rm -f gpurun_out/${TAG}_bench_paged.jsonl
 for P in 16 32 64 128; do timeout 300 python bench.py --no-cpu-baseline --paged $P >> gpurun_out/${TAG}_bench_paged.jsonl 2>/dev/null; done; echo "paged done"
-for C in mla16_b16_ctx32k mqa64_b32_ctx32k; do timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-a5 --config $C >> gpurun_out/${TAG}_bench_variants.jsonl 2>/dev/null; done; echo "variants done"
+for C in qwen3-8b_b32_ctx32k mla16_b16_ctx32k mqa64_b32_ctx32k; do timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-a5 --config $C >> gpurun_out/${TAG}_bench_variants.jsonl 2>/dev/null; done; echo "variants done"

@@ -6,8 +6,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2510_07486_b200 import build as asp_build
 _extra = os.environ.get("SEL_DEFINES", "").split()
-os.environ["ASYNCSPADE_LIB"] = asp_build.build_profiling(["-DASP_PROFILE_SELECT", *_extra],
-                                                         tag="prof" + "".join(d.replace("-D", "_") for d in _extra))
+os.environ["ASYNCSPADE_LIB"] = os.environ.get("PROF_LIB") or asp_build.build_profiling(
+    ["-DASP_PROFILE_SELECT", *_extra], tag="prof" + "".join(d.replace("-D", "_") for d in _extra))
 print("select defines:", _extra or "(default)")
 import torch
 import paper_2510_07486_b200 as asp

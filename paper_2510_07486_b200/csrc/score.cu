@@ -580,35 +580,64 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
             const int b = row / p.n_kv_heads, h = row % p.n_kv_heads;
             const float *qsrc = q_hat + ((size_t)b * p.n_q_heads + (size_t)h * G) * D;
             unsigned char *slot = gbslot0 + bs * C::kBSlotBytes;
-            // one 16-B chunk (8 consecutive d of one B row) per lane-iteration
-            constexpr int kChunks = N * D / 8;
-            for (int c = lane; c < kChunks; c += 32) {
-                const int n = c / (D / 8), d0 = (c % (D / 8)) * 8;
-                uint32_t w[4] = {0u, 0u, 0u, 0u};
-                if (n < 3 * G) {
-                    const int g = n % G, term = n / G;
-                    const float4 x0 = *reinterpret_cast<const float4 *>(qsrc + g * D + d0);
-                    const float4 x1 = *reinterpret_cast<const float4 *>(qsrc + g * D + d0 + 4);
-                    const float xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-                    uint16_t hv[8];
-#pragma unroll
-                    for (int e = 0; e < 8; e++) {
-                        // exact 3-way split q = hi + mid + lo (each residual is exact in fp32)
-                        const float q = xs[e];
-                        const __nv_bfloat16 hi = __float2bfloat16_rn(q);
-                        const float r1 = q - __bfloat162float(hi);
-                        const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-                        const float r2 = r1 - __bfloat162float(mid);
-                        const __nv_bfloat16 lo = __float2bfloat16_rn(r2);
-                        const __nv_bfloat16 t = term == 0 ? hi : term == 1 ? mid : lo;
-                        hv[e] = *reinterpret_cast<const uint16_t *>(&t);
-                    }
-#pragma unroll
-                    for (int e = 0; e < 4; e++) w[e] = (uint32_t)hv[2 * e] | ((uint32_t)hv[2 * e + 1] << 16);
-                }
+            // One (head g, 8 consecutive d) pair per lane-iteration: ONE load of q_hat
+            // feeds the pair's three 16-B chunks (rows g, G + g, 2G + g: the hi /
+            // mid / lo terms), and the loads of kBatch iterations are issued before
+            // any is used -- the row's first MMA waits for this build (at G = 64 a
+            // load-use loop over the 3G x D chunks cost ~37 us per CTA).
+            auto put = [&](int n, int d0, uint4 w) {
                 const int region = d0 / 64, chunk = (d0 % 64) / 8;
-                const int off = region * C::kBRegionBytes + n * 128 + ((chunk ^ (n & 7)) * 16);
-                *reinterpret_cast<uint4 *>(slot + off) = make_uint4(w[0], w[1], w[2], w[3]);
+                *reinterpret_cast<uint4 *>(slot + region * C::kBRegionBytes + n * 128 +
+                                           ((chunk ^ (n & 7)) * 16)) = w;
+            };
+            for (int c = lane; c < (N - 3 * G) * (D / 8); c += 32)        // padding rows: zero
+                put(3 * G + c / (D / 8), (c % (D / 8)) * 8, make_uint4(0u, 0u, 0u, 0u));
+            constexpr int kPairs = G * D / 8;
+            constexpr int kPer = (kPairs + 31) / 32;                      // iterations per lane
+            constexpr int kBatch = kPer < 8 ? kPer : 8;
+            for (int p0 = 0; p0 < kPer; p0 += kBatch) {
+                float4 x0[kBatch], x1[kBatch];
+#pragma unroll
+                for (int u = 0; u < kBatch; u++) {
+                    const int pc = lane + 32 * (p0 + u);
+                    if (pc < kPairs) {
+                        const int g = pc / (D / 8), d0 = (pc % (D / 8)) * 8;
+                        x0[u] = *reinterpret_cast<const float4 *>(qsrc + g * D + d0);
+                        x1[u] = *reinterpret_cast<const float4 *>(qsrc + g * D + d0 + 4);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kBatch; u++) {
+                    const int pc = lane + 32 * (p0 + u);
+                    if (pc >= kPairs) continue;
+                    const int g = pc / (D / 8), d0 = (pc % (D / 8)) * 8;
+                    const float xs[8] = {x0[u].x, x0[u].y, x0[u].z, x0[u].w,
+                                         x1[u].x, x1[u].y, x1[u].z, x1[u].w};
+                    uint32_t wh[4], wm[4], wl[4];
+#pragma unroll
+                    for (int e = 0; e < 8; e += 2) {
+                        uint16_t hv[2], mv[2], lv[2];
+#pragma unroll
+                        for (int f = 0; f < 2; f++) {
+                            // exact 3-way split q = hi + mid + lo (each residual is exact in fp32)
+                            const float q = xs[e + f];
+                            const __nv_bfloat16 hi = __float2bfloat16_rn(q);
+                            const float r1 = q - __bfloat162float(hi);
+                            const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+                            const float r2 = r1 - __bfloat162float(mid);
+                            const __nv_bfloat16 lo = __float2bfloat16_rn(r2);
+                            hv[f] = *reinterpret_cast<const uint16_t *>(&hi);
+                            mv[f] = *reinterpret_cast<const uint16_t *>(&mid);
+                            lv[f] = *reinterpret_cast<const uint16_t *>(&lo);
+                        }
+                        wh[e / 2] = (uint32_t)hv[0] | ((uint32_t)hv[1] << 16);
+                        wm[e / 2] = (uint32_t)mv[0] | ((uint32_t)mv[1] << 16);
+                        wl[e / 2] = (uint32_t)lv[0] | ((uint32_t)lv[1] << 16);
+                    }
+                    put(g, d0, make_uint4(wh[0], wh[1], wh[2], wh[3]));
+                    put(G + g, d0, make_uint4(wm[0], wm[1], wm[2], wm[3]));
+                    put(2 * G + g, d0, make_uint4(wl[0], wl[1], wl[2], wl[3]));
+                }
             }
             fence_proxy_async_smem();
             __syncwarp();

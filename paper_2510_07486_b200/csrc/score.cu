@@ -23,7 +23,7 @@
 //     Warp roles: warp 0 streams K tiles
 //     with TMA (4-D tensor map over the strided cache, 128-B swizzle,
 //     L2 evict-first) into a 6-stage mbarrier ring; warp 1 owns TMEM and
-//     issues the MMAs (single thread); warp 2 builds the swizzled bf16 B
+//     issues the MMAs (single thread); warps 2-3 build the swizzled bf16 B
 //     operand for each new row into a 2-slot ring; warps 4-11 (two
 //     warpgroups alternating tiles) drain TMEM (tcgen05.ld, 6 accumulator
 //     stages) and store the fp32 scores.
@@ -337,7 +337,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::kStages; s++) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
         for (int a = 0; a < C::kAcc; a++) { mbar_init(tfull_bar(a), 1); mbar_init(tempty_bar(a), 4); }
-        for (int s = 0; s < C::kBSlots; s++) { mbar_init(bfull_bar(s), 1); mbar_init(bempty_bar(s), 1); }
+        for (int s = 0; s < C::kBSlots; s++) { mbar_init(bfull_bar(s), 2); mbar_init(bempty_bar(s), 1); }
         fence_mbar_init();
         prefetch_tmap(&kmap);
     }
@@ -565,8 +565,9 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
             PFLUSH(1, pm_full); PFLUSH(2, pm_tempty); PFLUSH(3, pm_issue); PFLUSH(7, pm_b);
         }
         __syncwarp();
-    } else if (warp == 2) {
-        // ------------------------------------------------ B-operand builder
+    } else if (warp == 2 || warp == 3) {
+        // ------------------------------------------------ B-operand builders (two warps)
+        const int bl = lane + 32 * (warp - 2);                // 0..63
         int bs = -1;
         uint32_t bph = 0;
         int cur_row = -1;
@@ -590,16 +591,16 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
                 *reinterpret_cast<uint4 *>(slot + region * C::kBRegionBytes + n * 128 +
                                            ((chunk ^ (n & 7)) * 16)) = w;
             };
-            for (int c = lane; c < (N - 3 * G) * (D / 8); c += 32)        // padding rows: zero
+            for (int c = bl; c < (N - 3 * G) * (D / 8); c += 64)          // padding rows: zero
                 put(3 * G + c / (D / 8), (c % (D / 8)) * 8, make_uint4(0u, 0u, 0u, 0u));
             constexpr int kPairs = G * D / 8;
-            constexpr int kPer = (kPairs + 31) / 32;                      // iterations per lane
+            constexpr int kPer = (kPairs + 63) / 64;                      // iterations per thread
             constexpr int kBatch = kPer < 8 ? kPer : 8;
             for (int p0 = 0; p0 < kPer; p0 += kBatch) {
                 float4 x0[kBatch], x1[kBatch];
 #pragma unroll
                 for (int u = 0; u < kBatch; u++) {
-                    const int pc = lane + 32 * (p0 + u);
+                    const int pc = bl + 64 * (p0 + u);
                     if (pc < kPairs) {
                         const int g = pc / (D / 8), d0 = (pc % (D / 8)) * 8;
                         x0[u] = *reinterpret_cast<const float4 *>(qsrc + g * D + d0);
@@ -608,7 +609,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap kmap, asp_select_params p,
                 }
 #pragma unroll
                 for (int u = 0; u < kBatch; u++) {
-                    const int pc = lane + 32 * (p0 + u);
+                    const int pc = bl + 64 * (p0 + u);
                     if (pc >= kPairs) continue;
                     const int g = pc / (D / 8), d0 = (pc % (D / 8)) * 8;
                     const float xs[8] = {x0[u].x, x0[u].y, x0[u].z, x0[u].w,

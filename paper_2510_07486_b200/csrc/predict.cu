@@ -800,6 +800,9 @@ predict_split_kernel(asp_predict_params p, const float *__restrict__ q_window,
     asp::pdl_trigger();              // window read before the wait: see predict_pair_kernel
     const bool has1 = row0 + 1 < rows;
     const int rs = p.ring_start;
+#ifdef ASP_PROFILE_PREDICT
+    long long _tp = clock64();
+#endif
     auto phys_of = [&](int i) {
         const int ph = i + rs;
         return ph >= W ? ph - W : ph;
@@ -860,6 +863,7 @@ predict_split_kernel(asp_predict_params p, const float *__restrict__ q_window,
                     }
                 }
     }
+    PPROF(0);
     __syncthreads();
     // sum the slices in warp order into sP[0]
     for (int x = threadIdx.x; x < 2 * 16 * kGS; x += kSplit * 32) {
@@ -882,7 +886,9 @@ predict_split_kernel(asp_predict_params p, const float *__restrict__ q_window,
         }
     }
     __syncthreads();
+    PPROF(1);
     asp::pdl_wait();                 // q_hat / flags written from here on
+    PPROF(2);
     // ---- q_hat slice = (1/m) sum_p c_p Q[p]: each lane weights its two rows,
     // the 8 lanes of a column (same fc) reduce by shuffle
 #pragma unroll
@@ -925,6 +931,7 @@ predict_split_kernel(asp_predict_params p, const float *__restrict__ q_window,
             if (threadIdx.x == 0) asp::flag_or(dev_flags, st == 2 ? ASP_FLAG_NOT_PD : ASP_FLAG_NONFINITE);
         }
     }
+    PPROF(3);
 }
 
 template <int D, int NB>

@@ -873,6 +873,7 @@ predict_split_kernel(asp_predict_params p, const float *__restrict__ q_window,
         (&sP[0][0][0])[x] = v;
     }
     __syncthreads();
+    PPROF(4);
     // ---- Steps 3-6: warp 0 solves both rows (one per half-warp)
     if (warp == 0) {
         const int h = lane >> 4, l = lane & 15;

@@ -29,8 +29,9 @@ for name, P, warps_per_row in [("qwen3-32b_b64_ctx32k", 1, 0.5), ("qwen3-32b_b64
     rows = cfg.batch * cfg.n_q_heads // P
     warps = rows * warps_per_row
     print(f"{name} P={P}: {rows} query rows, {warps:.0f} warps")
-    for i in range(4):
-        print(f"  phase {i}: {buf[i] / warps / 1965:8.2f} us per warp")
+    for i, nm in [(0, "window + Gram"), (4, "slice sum (split)"), (1, "solve (+ sync)"),
+                  (2, "pdl wait"), (3, "weighted sum + store")]:
+        print(f"  {nm:22s} {buf[i] / warps / 1965:8.2f} us per warp")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(20):

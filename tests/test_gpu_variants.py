@@ -53,15 +53,18 @@ def test_score_select_wide_shapes(D, G):
             check_selection(idx[b, h], so[b, h], n, k)
 
 
-@pytest.mark.parametrize("D,Dv,G,n_fresh", [(576, 512, 16, 0), (576, 512, 16, 1), (576, 512, 1, 1),
-                                            (128, 128, 64, 1), (128, 128, 128, 0),
-                                            (64, 64, 64, 3)])
-def test_decode_wide_shapes(D, Dv, G, n_fresh):
+@pytest.mark.parametrize("D,Dv,G,n_fresh,Hkv", [(576, 512, 16, 0, 1), (576, 512, 16, 1, 1),
+                                                (576, 512, 1, 1, 1), (128, 128, 64, 1, 1),
+                                                (128, 128, 128, 0, 1), (64, 64, 64, 3, 1),
+                                                (128, 128, 64, 1, 2)])
+def test_decode_wide_shapes(D, Dv, G, n_fresh, Hkv):
     """Sparse decode for absorbed MLA (V = the first 512 dims of the key rows,
-    one cache) and MQA with 64 / 128 heads: within 2e-3 of the oracle, 3
-    chunks with -1 padding and the fresh tail."""
-    rng = np.random.default_rng(D + G + n_fresh)
-    B, Hkv, L, k = 2, 1, 1500, 600
+    one cache) and 64 / 128 query heads per KV head -- on the tensor cores as
+    virtual KV heads when there is one KV head (MQA), on the CUDA cores with
+    two: within 2e-3 of the oracle, 3 chunks with -1 padding and the fresh
+    tail."""
+    rng = np.random.default_rng(D + G + n_fresh + Hkv)
+    B, L, k = 2, 1500, 600
     lens = [1500, 900]
     K = synth.kv_cache(77 + D, synth.STREAM_K, B, Hkv, L, D)
     mla = Dv < D
@@ -70,7 +73,8 @@ def test_decode_wide_shapes(D, Dv, G, n_fresh):
     idx = np.full((B, Hkv, k), -1, np.int32)
     for b in range(B):
         m = min(k - 7, lens[b])
-        idx[b, 0, :m] = np.sort(rng.choice(lens[b], m, replace=False))
+        for h in range(Hkv):
+            idx[b, h, :m] = np.sort(rng.choice(lens[b], m, replace=False))
     Kd = _dev(K)
     Vd = Kd if mla else _dev(V)
     p = asp.decode_params(_dev(q), Kd, Vd, k, n_fresh, v_head_dim=Dv if mla else 0)

@@ -316,7 +316,7 @@ predict_kernel(asp_predict_params p, const float *__restrict__ q_window,
     const int W = p.window, n = W - 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long rows = (long)p.batch * p.n_q_heads;
-    const long row = (long)blockIdx.x * kWarps + warp;
+    const long row = (long)blockIdx.x * (blockDim.x >> 5) + warp;   // 1..kWarps rows per CTA
     asp::pdl_wait();
     asp::pdl_trigger();
     if (row >= rows) return;
@@ -966,14 +966,18 @@ template <int D, int NB>
 cudaError_t launch(const asp_predict_params &p, const float *q_window, float *q_hat,
                    uint32_t *dev_flags, cudaStream_t s) {
     const long rows = (long)p.batch * p.n_q_heads;
-    const size_t smem = warp_smem_bytes(p.window) * kWarps;
+    // rows per CTA: kWarps, or fewer so that few rows (absorbed MLA's 256, say)
+    // still spread over twice the SMs instead of sharing a few SMs' fp64 pipes
+    int wpc = kWarps;
+    while (wpc > 1 && (rows + wpc - 1) / wpc < 2L * asp_sm_count()) wpc /= 2;
+    const size_t smem = warp_smem_bytes(p.window) * wpc;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(predict_kernel<D, NB>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    const unsigned grid = (unsigned)((rows + kWarps - 1) / kWarps);
-    return asp_launch(predict_kernel<D, NB>, dim3(grid), dim3(kWarps * 32), smem, s, 1, p, q_window,
+    const unsigned grid = (unsigned)((rows + wpc - 1) / wpc);
+    return asp_launch(predict_kernel<D, NB>, dim3(grid), dim3(wpc * 32), smem, s, 1, p, q_window,
                       q_hat, dev_flags);
 }
 

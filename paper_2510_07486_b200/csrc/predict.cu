@@ -781,15 +781,21 @@ predict_pair_kernel(asp_predict_params p, const float *__restrict__ q_window,
 // (deterministic), warp 0 solves both rows (solve_coeffs), and every warp
 // writes its slice of q_hat.  The latency chain is one DRAM round trip plus
 // the solve, instead of a row pair's whole window streamed through one warp.
-constexpr int kSplit = 4;
+// kSplit warps: 4 (D = 64 / 128 / 256), 12 for the 576-dim absorbed-MLA query
+// (three 16-dim groups per warp; the partial Grams then need dynamic smem).
+template <int D>
+constexpr int split_warps() { return D == 576 ? 12 : 4; }
 
 template <int D, int NB, bool BF>
-__global__ void __launch_bounds__(kSplit * 32)
+__global__ void __launch_bounds__(split_warps<D>() * 32)
 predict_split_kernel(asp_predict_params p, const float *__restrict__ q_window,
                      float *__restrict__ q_hat, uint32_t *dev_flags) {
-    constexpr int kG = D / (16 * kSplit);               // 16-dim groups per warp (2 or 1)
+    constexpr int kSplit = split_warps<D>();
+    constexpr int kG = D / (16 * kSplit);               // 16-dim groups per warp (2, 1 or 3)
+    static_assert(kG * 16 * kSplit == D, "head-dim slices");
     constexpr int T = NB * (NB + 1) / 2;
-    __shared__ double sP[kSplit][2][16 * kGS];         // partial augmented Grams
+    extern __shared__ double sP_raw[];
+    double (*sP)[2][16 * kGS] = reinterpret_cast<double (*)[2][16 * kGS]>(sP_raw);   // partial Grams
     __shared__ double sC[2][16];                       // c_{l+1} per row
     __shared__ double sDen[2];
     __shared__ int sOk[2];
@@ -941,7 +947,13 @@ cudaError_t launch_split(const asp_predict_params &p, const float *q_window, flo
     auto kern = (p.flags & ASP_WINDOW_BF16) ? predict_split_kernel<D, NB, true>
                                             : predict_split_kernel<D, NB, false>;
     const long rows = (long)p.batch * p.n_q_heads;
-    return asp_launch(kern, dim3((unsigned)((rows + 1) / 2)), dim3(kSplit * 32), 0, s, 1, p,
+    constexpr int kSplit = split_warps<D>();
+    const int smem = (int)(sizeof(double) * kSplit * 2 * 16 * kGS);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+    }
+    return asp_launch(kern, dim3((unsigned)((rows + 1) / 2)), dim3(kSplit * 32), smem, s, 1, p,
                       q_window, q_hat, dev_flags);
 }
 
@@ -1001,6 +1013,12 @@ cudaError_t asp_launch_predict(const asp_predict_params &p, const float *q_windo
                                                  : launch_split<64, 2>(p, q_window, q_hat, dev_flags, s);
             if (p.head_dim == 128) return nb == 1 ? launch_split<128, 1>(p, q_window, q_hat, dev_flags, s)
                                                   : launch_split<128, 2>(p, q_window, q_hat, dev_flags, s);
+            // wide queries (absorbed MLA's 576-dim latent, 256-dim heads): the same
+            // slicing over 12 / 4 warps instead of a whole window per warp
+            if (p.head_dim == 576) return nb == 1 ? launch_split<576, 1>(p, q_window, q_hat, dev_flags, s)
+                                                  : launch_split<576, 2>(p, q_window, q_hat, dev_flags, s);
+            if (p.head_dim == 256) return nb == 1 ? launch_split<256, 1>(p, q_window, q_hat, dev_flags, s)
+                                                  : launch_split<256, 2>(p, q_window, q_hat, dev_flags, s);
         }
         if (p.head_dim == 64) return nb == 1 ? launch_pair<64, 1>(p, q_window, q_hat, dev_flags, s)
                                              : launch_pair<64, 2>(p, q_window, q_hat, dev_flags, s);
